@@ -1,0 +1,434 @@
+// oracle/hjo.cpp — CPU ORACLE. TEST INFRASTRUCTURE ONLY.
+//
+// Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+// reference legs may load this library.  The product path
+// (paper_2006_16465_b200/) never links, imports or calls it, and shares no code,
+// header, table or constant generator with it.
+//
+// What it computes: classic Jacobi and the paper's hierarchical ("shared-memory")
+// Jacobi for the 1D 3-point and 2D 5-point Poisson problem, written as plain,
+// slow, single-threaded loops that follow the paper step by step:
+//   * Jacobi splitting / elemental update      PAPER.md:29-37  (§2.1, Eqs. 1-2)
+//   * 1D Poisson system and update             PAPER.md:180-212 (§3.4, Eqs. 5-7)
+//   * 2D Poisson system and update             PAPER.md:393-421 (§4.2)
+//   * CPU approach (two arrays, swap)          PAPER.md:94-112  (§3.1 listing)
+//   * hierarchical cycle: copy tile+halo, k sub-iterations with frozen halo,
+//     write the interior back                  PAPER.md:161-166 (§3.3), :382-387 (§4.1),
+//                                              Appendix A
+//   * stopping rule: reduce the L2 residual of the initial solution by a factor
+//     (relative test)
+//   * resource figures (shared bytes, blocks)
+//
+// Readings where the paper is silent/garbled are SURVEY.md §8(c) c1..c18, listed
+// in DESIGN.md §3.  In particular:
+//   c6  snapshot semantics: a cycle reads x_c and writes x_{c+1} into a second array
+//       (Appendix A writes in place, a race — PAPER.md:549, :573);
+//   c7  the rhs of the updated cell is used (Appendix A's rhs index is off by one);
+//   c8  the write-back takes the values after exactly k sub-iterations (odd k too);
+//   c10 ragged last tile when n is not a multiple of the tile;
+//   c12 the Dirichlet ring may hold non-zero values g;
+//   c3  the residual is computed in the h^2-scaled form
+//       s = h^2 f - (2x - (x_{i-1}+x_{i+1}))            (1D)
+//       s = h^2 f - (4x - ((xW+xE)+(xS+xN)))            (2D)
+//       in double, ||b - Ax||_2 = sqrt(sum s^2) / h^2;
+//   c16 fp32 iterates: h2f = float(h*h*f) (one rounding of the double product),
+//       update in fp32 with the same expression; the residual uses the double
+//       product h*h*f and the iterate converted to double.
+//
+// Canonical arithmetic: the elemental update of
+// PAPER.md:210 / :420 is evaluated exactly as
+//       1D: T(0.5)  * ((xL + xR) + h2f)
+//       2D: T(0.25) * (((xW + xE) + (xS + xN)) + h2f)
+// Built with -O2 -ffp-contract=off (no FMA contraction, no fast-math).
+//
+// Layout: interior arrays are row-major, x fastest.
+// Internally every grid carries its Dirichlet ring: (nx+2) x (ny+2) values,
+// index (j)*(nx+2) + i with i = 0..nx+1 along x and j = 0..ny+1 along y
+// (1D: nx+2 values).  Ring corners are never read by the 5-point stencil.
+//
+// Boundary-data layout ("bc"), shared with the ABI only by documentation:
+//   1D: [g_left, g_right]
+//   2D: [south(nx) | north(nx) | west(ny) | east(ny)]   (south = row y=0)
+//   NULL means homogeneous (the paper's u = 0).
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+#include <algorithm>
+
+namespace {
+
+// ---------------------------------------------------------------- 1D ----------
+
+// Elemental Jacobi update for -u'' = f, PAPER.md:210 (Eq. jacobi-stencil-1d-poisson):
+//     x_i <- (b_i dx^2 + x_{i-1} + x_{i+1}) / 2
+template <typename T>
+inline T update1d(T left, T right, T h2f) {
+  return T(0.5) * ((left + right) + h2f);
+}
+
+// Residual contribution in the h^2-scaled form (reading c3), always double.
+inline double resid1d(double x, double left, double right, double h2f64) {
+  return h2f64 - (2.0 * x - (left + right));
+}
+
+template <typename T>
+struct Problem1D {
+  int64_t n;                 // interior points (paper's N)
+  double h2;                 // h*h
+  std::vector<T> h2f;        // T(h2*f_i), i = 0..n-1 (interior index)
+  std::vector<double> h2f64; // h2*f_i in double (true rhs for the residual)
+  T gl, gr;                  // Dirichlet values at x=0 and x=1
+};
+
+// x has n+2 entries: x[0] = g_left, x[1..n] interior, x[n+1] = g_right.
+template <typename T>
+double residual_sq_1d(const Problem1D<T>& p, const std::vector<T>& x) {
+  double S = 0.0;
+  for (int64_t i = 1; i <= p.n; ++i) {
+    double s = resid1d((double)x[i], (double)x[i - 1], (double)x[i + 1], p.h2f64[i - 1]);
+    S += s * s;
+  }
+  return S;
+}
+
+// §3.1 CPU approach: every DOF from the previous iterate.
+template <typename T>
+void classic_sweep_1d(const Problem1D<T>& p, const std::vector<T>& x0, std::vector<T>& x1) {
+  for (int64_t i = 1; i <= p.n; ++i)
+    x1[i] = update1d<T>(x0[i - 1], x0[i + 1], p.h2f[i - 1]);
+}
+
+// §3.3 hierarchical cycle, 1D (Appendix A :548-573), o = 0.
+// Tile t covers interior points [1 + t*T, min((t+1)*T, n)] (ragged last tile, c10).
+// tile_order = 0: tiles in increasing order; 1: decreasing (used by the
+// order-independence test — the result must not depend on it).
+template <typename T>
+void hier_cycle_1d(const Problem1D<T>& p, int64_t tile, int k, int tile_order,
+                   const std::vector<T>& xc, std::vector<T>& xn) {
+  const int64_t ntiles = (p.n + tile - 1) / tile;
+  std::vector<T> A, B, rhs;
+  for (int64_t tt = 0; tt < ntiles; ++tt) {
+    const int64_t t = tile_order == 0 ? tt : ntiles - 1 - tt;
+    const int64_t lo = 1 + t * tile;                  // first interior point
+    const int64_t hi = std::min((t + 1) * tile, p.n); // last interior point
+    const int64_t w = hi - lo + 1;
+    // Step 1: copy the augmented subdomain [lo-1, hi+1] into two containers,
+    // and the rhs of the interior points.
+    A.assign(xc.begin() + (lo - 1), xc.begin() + (hi + 2));
+    B = A;
+    rhs.assign(p.h2f.begin() + (lo - 1), p.h2f.begin() + hi);
+    // Step 2: k sub-iterations on the interior; the two halo points are never
+    // written (frozen at snapshot values, reading c5).
+    for (int q = 0; q < k; ++q) {
+      for (int64_t i = 1; i <= w; ++i) B[i] = update1d<T>(A[i - 1], A[i + 1], rhs[i - 1]);
+      std::swap(A, B);
+    }
+    // Step 3: write the latest interior values into the NEXT global array
+    // (snapshot semantics c6; latest values c8).
+    for (int64_t i = 1; i <= w; ++i) xn[lo - 1 + i] = A[i];
+  }
+}
+
+// ---------------------------------------------------------------- 2D ----------
+
+// Elemental Jacobi update for -(u_xx + u_yy) = f with dx = dy = h,
+// x_ij <- (b_ij h^2 + x_{i-1,j} + x_{i+1,j} + x_{i,j-1} + x_{i,j+1}) / 4
+template <typename T>
+inline T update2d(T w, T e, T s, T n, T h2f) {
+  return T(0.25) * (((w + e) + (s + n)) + h2f);
+}
+
+inline double resid2d(double x, double w, double e, double s, double n, double h2f64) {
+  return h2f64 - (4.0 * x - ((w + e) + (s + n)));
+}
+
+template <typename T>
+struct Problem2D {
+  int64_t nx, ny;
+  double h2;
+  std::vector<T> h2f;        // nx*ny, row-major
+  std::vector<double> h2f64; // nx*ny
+  int64_t pitch() const { return nx + 2; }
+};
+
+// index of (i, j) in a ringed grid, i = 0..nx+1 (x), j = 0..ny+1 (y)
+template <typename T>
+inline int64_t at(const Problem2D<T>& p, int64_t i, int64_t j) { return j * p.pitch() + i; }
+
+template <typename T>
+double residual_sq_2d(const Problem2D<T>& p, const std::vector<T>& x) {
+  double S = 0.0;
+  for (int64_t j = 1; j <= p.ny; ++j)
+    for (int64_t i = 1; i <= p.nx; ++i) {
+      double s = resid2d((double)x[at(p, i, j)], (double)x[at(p, i - 1, j)], (double)x[at(p, i + 1, j)],
+                         (double)x[at(p, i, j - 1)], (double)x[at(p, i, j + 1)],
+                         p.h2f64[(j - 1) * p.nx + (i - 1)]);
+      S += s * s;
+    }
+  return S;
+}
+
+template <typename T>
+void classic_sweep_2d(const Problem2D<T>& p, const std::vector<T>& x0, std::vector<T>& x1) {
+  for (int64_t j = 1; j <= p.ny; ++j)
+    for (int64_t i = 1; i <= p.nx; ++i)
+      x1[at(p, i, j)] = update2d<T>(x0[at(p, i - 1, j)], x0[at(p, i + 1, j)], x0[at(p, i, j - 1)],
+                                    x0[at(p, i, j + 1)], p.h2f[(j - 1) * p.nx + (i - 1)]);
+}
+
+// §4.1 hierarchical cycle, 2D, o = 0.  Tile (a, b) covers
+// interior x in [1 + a*Tx, min((a+1)*Tx, nx)], y in [1 + b*Ty, min((b+1)*Ty, ny)].
+// The augmented subdomain is (w+2) x (hgt+2); the halo is frozen.
+template <typename T>
+void hier_cycle_2d(const Problem2D<T>& p, int64_t tx, int64_t ty, int k, int tile_order,
+                   const std::vector<T>& xc, std::vector<T>& xn) {
+  const int64_t ntx = (p.nx + tx - 1) / tx, nty = (p.ny + ty - 1) / ty;
+  const int64_t ntiles = ntx * nty;
+  std::vector<T> A, B, rhs;
+  for (int64_t tt = 0; tt < ntiles; ++tt) {
+    const int64_t t = tile_order == 0 ? tt : ntiles - 1 - tt;
+    const int64_t a = t % ntx, b = t / ntx;
+    const int64_t ilo = 1 + a * tx, ihi = std::min((a + 1) * tx, p.nx);
+    const int64_t jlo = 1 + b * ty, jhi = std::min((b + 1) * ty, p.ny);
+    const int64_t w = ihi - ilo + 1, hgt = jhi - jlo + 1, lp = w + 2;
+    // Step 1: copy the augmented subdomain (two containers) and the local rhs.
+    A.assign((size_t)(lp * (hgt + 2)), T(0));
+    for (int64_t jj = 0; jj < hgt + 2; ++jj)
+      for (int64_t ii = 0; ii < lp; ++ii) A[jj * lp + ii] = xc[at(p, ilo - 1 + ii, jlo - 1 + jj)];
+    B = A;
+    rhs.assign((size_t)(w * hgt), T(0));
+    for (int64_t jj = 0; jj < hgt; ++jj)
+      for (int64_t ii = 0; ii < w; ++ii)
+        rhs[jj * w + ii] = p.h2f[(jlo - 1 + jj) * p.nx + (ilo - 1 + ii)];
+    // Step 2: k sub-iterations on the interior, halo frozen.
+    for (int q = 0; q < k; ++q) {
+      for (int64_t jj = 1; jj <= hgt; ++jj)
+        for (int64_t ii = 1; ii <= w; ++ii)
+          B[jj * lp + ii] = update2d<T>(A[jj * lp + ii - 1], A[jj * lp + ii + 1], A[(jj - 1) * lp + ii],
+                                        A[(jj + 1) * lp + ii], rhs[(jj - 1) * w + (ii - 1)]);
+      std::swap(A, B);
+    }
+    // Step 3: write the interior into the next global array.
+    for (int64_t jj = 1; jj <= hgt; ++jj)
+      for (int64_t ii = 1; ii <= w; ++ii) xn[at(p, ilo - 1 + ii, jlo - 1 + jj)] = A[jj * lp + ii];
+  }
+}
+
+// ------------------------------------------------------------- driver ---------
+// SURVEY.md §8(c) step 6.  S_0 = S(x_0) (or (ref_residual*h2)^2).  hist[0].
+// If S_0 == 0 return c = 0.  For c = 1..max_cycles: x_c, S_c, hist[c];
+// non-finite -> status 4; sqrt(S_c) <= tol*sqrt(S_0) -> converged at c.
+// Absolute mode: sqrt(S_c)/h2 <= tol.
+
+enum { ST_OK = 0, ST_NOT_CONVERGED = 1, ST_INVALID = 2, ST_NUMERIC = 4 };
+
+struct DriverOut {
+  int64_t cycles = 0;
+  int converged = 0;
+  int status = ST_OK;
+};
+
+template <typename Cycle, typename Resid>
+DriverOut drive(double h2, double tol, int tol_mode, double ref_residual, int64_t max_cycles,
+                double* hist, Cycle&& cycle, Resid&& resid) {
+  DriverOut out;
+  double S0 = resid();
+  double sqrtS0 = ref_residual > 0.0 ? ref_residual * h2 : std::sqrt(S0);
+  if (hist) hist[0] = std::sqrt(S0) / h2;
+  if (!std::isfinite(S0)) { out.status = ST_NUMERIC; return out; }
+  auto test = [&](double S) {
+    return tol_mode == 0 ? (std::sqrt(S) <= tol * sqrtS0) : (std::sqrt(S) / h2 <= tol);
+  };
+  if (S0 == 0.0 || (ref_residual > 0.0 && test(S0)) || (tol_mode == 1 && test(S0))) {
+    out.converged = 1;
+    out.cycles = 0;
+    return out;
+  }
+  for (int64_t c = 1; c <= max_cycles; ++c) {
+    cycle();
+    double S = resid();
+    if (hist) hist[c] = std::sqrt(S) / h2;
+    out.cycles = c;
+    if (!std::isfinite(S)) { out.status = ST_NUMERIC; return out; }
+    if (test(S)) { out.converged = 1; return out; }
+  }
+  out.status = ST_NOT_CONVERGED;
+  return out;
+}
+
+template <typename T>
+int solve1d(int64_t n, double h, const double* f, const double* bc, const double* x0, int mode,
+            int64_t tile, int k, double tol, int tol_mode, double ref_residual, int64_t max_cycles,
+            int tile_order, double* x_out, double* hist, int64_t* cycles, int* converged) {
+  Problem1D<T> p;
+  p.n = n;
+  p.h2 = h * h;
+  p.h2f.resize(n);
+  p.h2f64.resize(n);
+  for (int64_t i = 0; i < n; ++i) {
+    p.h2f64[i] = p.h2 * f[i];
+    p.h2f[i] = (T)p.h2f64[i];
+  }
+  std::vector<T> xa(n + 2), xb(n + 2);
+  xa[0] = xb[0] = bc ? (T)bc[0] : T(0);
+  xa[n + 1] = xb[n + 1] = bc ? (T)bc[1] : T(0);
+  for (int64_t i = 0; i < n; ++i) xa[i + 1] = x0 ? (T)x0[i] : T(0);
+  std::vector<T>* cur = &xa;
+  std::vector<T>* nxt = &xb;
+  auto cycle = [&]() {
+    if (mode == 1) classic_sweep_1d(p, *cur, *nxt);
+    else hier_cycle_1d(p, tile, k, tile_order, *cur, *nxt);
+    std::swap(cur, nxt);
+  };
+  auto resid = [&]() { return residual_sq_1d(p, *cur); };
+  DriverOut o = drive(p.h2, tol, tol_mode, ref_residual, max_cycles, hist, cycle, resid);
+  for (int64_t i = 0; i < n; ++i) x_out[i] = (double)(*cur)[i + 1];
+  *cycles = o.cycles;
+  *converged = o.converged;
+  return o.status;
+}
+
+template <typename T>
+int solve2d(int64_t nx, int64_t ny, double h, const double* f, const double* bc, const double* x0,
+            int mode, int64_t tx, int64_t ty, int k, double tol, int tol_mode, double ref_residual,
+            int64_t max_cycles, int tile_order, double* x_out, double* hist, int64_t* cycles,
+            int* converged) {
+  Problem2D<T> p;
+  p.nx = nx;
+  p.ny = ny;
+  p.h2 = h * h;
+  p.h2f.resize(nx * ny);
+  p.h2f64.resize(nx * ny);
+  for (int64_t q = 0; q < nx * ny; ++q) {
+    p.h2f64[q] = p.h2 * f[q];
+    p.h2f[q] = (T)p.h2f64[q];
+  }
+  std::vector<T> xa((nx + 2) * (ny + 2), T(0));
+  // Dirichlet ring (reading c12): south row j=0, north row j=ny+1, west col i=0, east col i=nx+1
+  if (bc) {
+    for (int64_t i = 1; i <= nx; ++i) {
+      xa[at(p, i, 0)] = (T)bc[i - 1];
+      xa[at(p, i, ny + 1)] = (T)bc[nx + i - 1];
+    }
+    for (int64_t j = 1; j <= ny; ++j) {
+      xa[at(p, 0, j)] = (T)bc[2 * nx + j - 1];
+      xa[at(p, nx + 1, j)] = (T)bc[2 * nx + ny + j - 1];
+    }
+  }
+  std::vector<T> xb = xa;  // both arrays carry the ring
+  for (int64_t j = 1; j <= ny; ++j)
+    for (int64_t i = 1; i <= nx; ++i) xa[at(p, i, j)] = x0 ? (T)x0[(j - 1) * nx + (i - 1)] : T(0);
+  std::vector<T>* cur = &xa;
+  std::vector<T>* nxt = &xb;
+  auto cycle = [&]() {
+    if (mode == 1) classic_sweep_2d(p, *cur, *nxt);
+    else hier_cycle_2d(p, tx, ty, k, tile_order, *cur, *nxt);
+    std::swap(cur, nxt);
+  };
+  auto resid = [&]() { return residual_sq_2d(p, *cur); };
+  DriverOut o = drive(p.h2, tol, tol_mode, ref_residual, max_cycles, hist, cycle, resid);
+  for (int64_t j = 1; j <= ny; ++j)
+    for (int64_t i = 1; i <= nx; ++i) x_out[(j - 1) * nx + (i - 1)] = (double)(*cur)[at(p, i, j)];
+  *cycles = o.cycles;
+  *converged = o.converged;
+  return o.status;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Solve -Δu = f with classic (mode 1) or hierarchical (mode 0) Jacobi.
+// dim 1: ny must be 1 and tile_y is ignored.  dtype 0 = double, 1 = float.
+// x_out: nx*ny doubles.  hist: max_cycles+1 doubles or NULL.
+// Returns 0 converged, 1 not converged, 2 invalid argument, 4 non-finite residual.
+int hjo_solve(int dim, int64_t nx, int64_t ny, double h, const double* f, const double* bc,
+              const double* x0, int mode, int dtype, int64_t tile_x, int64_t tile_y, int k,
+              double tol, int tol_mode, double ref_residual, int64_t max_cycles, int tile_order,
+              double* x_out, double* hist, int64_t* cycles, int* converged) {
+  if (!f || !x_out || !cycles || !converged) return ST_INVALID;
+  if (!(h > 0.0) || !std::isfinite(h) || nx < 1 || ny < 1 || max_cycles < 0) return ST_INVALID;
+  if (mode != 0 && mode != 1) return ST_INVALID;
+  if (mode == 0 && (k < 1 || tile_x < 1 || tile_x > nx)) return ST_INVALID;
+  if (dim == 1) {
+    if (ny != 1) return ST_INVALID;
+    if (dtype == 0)
+      return solve1d<double>(nx, h, f, bc, x0, mode, tile_x, k, tol, tol_mode, ref_residual,
+                             max_cycles, tile_order, x_out, hist, cycles, converged);
+    return solve1d<float>(nx, h, f, bc, x0, mode, tile_x, k, tol, tol_mode, ref_residual,
+                          max_cycles, tile_order, x_out, hist, cycles, converged);
+  }
+  if (dim == 2) {
+    if (mode == 0 && (tile_y < 1 || tile_y > ny)) return ST_INVALID;
+    if (dtype == 0)
+      return solve2d<double>(nx, ny, h, f, bc, x0, mode, tile_x, tile_y, k, tol, tol_mode,
+                             ref_residual, max_cycles, tile_order, x_out, hist, cycles, converged);
+    return solve2d<float>(nx, ny, h, f, bc, x0, mode, tile_x, tile_y, k, tol, tol_mode,
+                          ref_residual, max_cycles, tile_order, x_out, hist, cycles, converged);
+  }
+  return ST_INVALID;
+}
+
+// ||f - A x||_2 for interior x (double), A = (1/h^2) * stencil, ring from bc.
+double hjo_residual(int dim, int64_t nx, int64_t ny, double h, const double* f, const double* bc,
+                    const double* x) {
+  const double h2 = h * h;
+  if (dim == 1) {
+    Problem1D<double> p;
+    p.n = nx;
+    p.h2 = h2;
+    p.h2f64.resize(nx);
+    for (int64_t i = 0; i < nx; ++i) p.h2f64[i] = h2 * f[i];
+    std::vector<double> xx(nx + 2);
+    xx[0] = bc ? bc[0] : 0.0;
+    xx[nx + 1] = bc ? bc[1] : 0.0;
+    for (int64_t i = 0; i < nx; ++i) xx[i + 1] = x[i];
+    return std::sqrt(residual_sq_1d(p, xx)) / h2;
+  }
+  Problem2D<double> p;
+  p.nx = nx;
+  p.ny = ny;
+  p.h2 = h2;
+  p.h2f64.resize(nx * ny);
+  for (int64_t q = 0; q < nx * ny; ++q) p.h2f64[q] = h2 * f[q];
+  std::vector<double> xx((nx + 2) * (ny + 2), 0.0);
+  if (bc) {
+    for (int64_t i = 1; i <= nx; ++i) {
+      xx[at(p, i, 0)] = bc[i - 1];
+      xx[at(p, i, ny + 1)] = bc[nx + i - 1];
+    }
+    for (int64_t j = 1; j <= ny; ++j) {
+      xx[at(p, 0, j)] = bc[2 * nx + j - 1];
+      xx[at(p, nx + 1, j)] = bc[2 * nx + ny + j - 1];
+    }
+  }
+  for (int64_t j = 1; j <= ny; ++j)
+    for (int64_t i = 1; i <= nx; ++i) xx[at(p, i, j)] = x[(j - 1) * nx + (i - 1)];
+  return std::sqrt(residual_sq_2d(p, xx)) / h2;
+}
+
+// Resource figures (o = 0):
+//   tiles   = ceil(nx/Tx) [* ceil(ny/Ty)]            (Eq. 8/13 at o=0)
+//   threads = tiles * Tx [* Ty]                       (Eq. 9/14 at o=0: one thread per DOF)
+//   smem    = 8 * (2*(Tx+2) + Tx)            1D       (PAPER.md:175; 800 B at Tx=32, :215)
+//           = 8 * (2*(Tx+2)*(Ty+2) + Tx*Ty)  2D       (PAPER.md:389; 26,688 B at 32x32, :425)
+// bytes_per_value lets fp32 report 4-byte figures ("4 bytes for floats").
+int hjo_resource_figures(int dim, int64_t nx, int64_t ny, int64_t tx, int64_t ty,
+                         int64_t bytes_per_value, int64_t* tiles, int64_t* threads, int64_t* smem) {
+  if (tx < 1 || tx > nx) return ST_INVALID;
+  if (dim == 1) {
+    *tiles = (nx + tx - 1) / tx;
+    *threads = *tiles * tx;
+    *smem = bytes_per_value * (2 * (tx + 2) + tx);
+    return ST_OK;
+  }
+  if (dim != 2 || ty < 1 || ty > ny) return ST_INVALID;
+  *tiles = ((nx + tx - 1) / tx) * ((ny + ty - 1) / ty);
+  *threads = *tiles * tx * ty;
+  *smem = bytes_per_value * (2 * (tx + 2) * (ty + 2) + tx * ty);
+  return ST_OK;
+}
+
+}  // extern "C"

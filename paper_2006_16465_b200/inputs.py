@@ -1,0 +1,97 @@
+"""Seeded synthetic inputs shared by tests, bench.py and the oracle harness.
+
+This module holds NONE of the method's arithmetic: it only produces the
+problem data (h, f, boundary ring g, initial guess x0) that both the CUDA path
+and the CPU oracle consume.  Recipes:
+
+* ``P`` — the paper's workload: f = 1, x0 = 1, g = 0.
+* ``M`` — manufactured: f = pi^2 sin(pi x) (1D) or 2 pi^2 sin(pi x) sin(pi y)
+  (2D), x0 = 0, g = 0 (the north star's sin(pi x) check).
+* ``R`` — parity stress: f, x0 ~ U[-1, 1) from splitmix64(seed + linear index),
+  g ~ U[-1, 1) from the same stream offset by nx*ny.
+* ``Q`` — exact polynomial solutions the 3/5-point stencils reproduce exactly:
+  1D u = x^3 - x (f = -6x, g = 0); 2D u = x^2 + y^2 (f = -4, g = u on the
+  ring, non-zero Dirichlet data).  x0 = 0.
+
+Grid: h = 1/(nx+1); interior node i (0-based) sits at x = (i+1) h; in 2D the
+same h is used along y (the ABI has one spacing, "if dx = dy").
+Arrays are row-major with x fastest: f[j*nx + i].  The 2D ring layout is
+[south(nx) | north(nx) | west(ny) | east(ny)]; 1D is [g_left, g_right].
+"""
+from __future__ import annotations
+
+import numpy as np
+
+SEED = 2006164650
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def splitmix64(idx: np.ndarray) -> np.ndarray:
+    """splitmix64 of a uint64 counter array (vectorised, wrapping arithmetic)."""
+    with np.errstate(over="ignore"):
+        z = idx.astype(np.uint64) + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def uniform_pm1(start: int, count: int) -> np.ndarray:
+    """U[-1, 1) doubles from splitmix64(start + 0..count-1)."""
+    idx = np.arange(count, dtype=np.uint64) + np.uint64(start)
+    u = (splitmix64(idx) >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+    return 2.0 * u - 1.0
+
+
+def make_problem(protocol: str, dim: int, nx: int, ny: int | None = None, seed: int = SEED):
+    """Return dict(dim, nx, ny, h, f, bc, x0) as float64 numpy arrays."""
+    if dim == 1:
+        ny = 1
+    elif ny is None:
+        ny = nx
+    n = nx * ny
+    h = 1.0 / (nx + 1)
+    xs = (np.arange(nx, dtype=np.float64) + 1.0) * h
+    ys = (np.arange(ny, dtype=np.float64) + 1.0) * h
+    nbc = 2 if dim == 1 else 2 * nx + 2 * ny
+    bc = np.zeros(nbc)
+    if protocol == "P":
+        f = np.ones(n)
+        x0 = np.ones(n)
+    elif protocol == "M":
+        if dim == 1:
+            f = np.pi ** 2 * np.sin(np.pi * xs)
+        else:
+            f = (2.0 * np.pi ** 2 * np.outer(np.sin(np.pi * ys), np.sin(np.pi * xs))).reshape(-1)
+        x0 = np.zeros(n)
+    elif protocol == "R":
+        f = uniform_pm1(seed, n)
+        x0 = uniform_pm1(seed + 7 * n + 13, n)
+        bc = uniform_pm1(seed + n, nbc)
+    elif protocol == "Q":
+        if dim == 1:
+            f = -6.0 * xs
+        else:
+            f = np.full(n, -4.0)
+            xe = (np.arange(nx + 2, dtype=np.float64)) * h
+            ye = (np.arange(ny + 2, dtype=np.float64)) * h
+            south = xe[1:-1] ** 2 + ye[0] ** 2
+            north = xe[1:-1] ** 2 + ye[-1] ** 2
+            west = xe[0] ** 2 + ye[1:-1] ** 2
+            east = xe[-1] ** 2 + ye[1:-1] ** 2
+            bc = np.concatenate([south, north, west, east])
+        x0 = np.zeros(n)
+    else:
+        raise ValueError(f"unknown protocol {protocol!r}")
+    return dict(dim=dim, nx=nx, ny=ny, h=h, f=np.ascontiguousarray(f), bc=bc,
+                x0=np.ascontiguousarray(x0))
+
+
+def exact_solution_Q(dim: int, nx: int, ny: int | None = None) -> np.ndarray:
+    """Nodal values of protocol Q's exact solution (interior, row-major)."""
+    h = 1.0 / (nx + 1)
+    xs = (np.arange(nx, dtype=np.float64) + 1.0) * h
+    if dim == 1:
+        return xs ** 3 - xs
+    ny = nx if ny is None else ny
+    ys = (np.arange(ny, dtype=np.float64) + 1.0) * h
+    return (xs[None, :] ** 2 + ys[:, None] ** 2).reshape(-1)
