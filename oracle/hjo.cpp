@@ -32,8 +32,11 @@
 //       s = h^2 f - (4x - ((xW+xE)+(xS+xN)))            (2D)
 //       in double, ||b - Ax||_2 = sqrt(sum s^2) / h^2;
 //   c16 fp32 iterates: h2f = float(h*h*f) (one rounding of the double product),
-//       update in fp32 with the same expression; the residual uses the double
-//       product h*h*f and the iterate converted to double.
+//       update in fp32 with the same expression; the residual is accumulated in
+//       double from the iterate and that SAME rounded h2f widened to double, i.e.
+//       it is the residual of the system the fp32 iteration actually solves
+//       (c16: keeps fp32 at 12 B/cell; differs from the true rhs by
+//       at most one fp32 rounding of h^2 f, far below the fp32 residual floor).
 //
 // Canonical arithmetic: the elemental update of
 // PAPER.md:210 / :420 is evaluated exactly as
@@ -78,7 +81,7 @@ struct Problem1D {
   int64_t n;                 // interior points (paper's N)
   double h2;                 // h*h
   std::vector<T> h2f;        // T(h2*f_i), i = 0..n-1 (interior index)
-  std::vector<double> h2f64; // h2*f_i in double (true rhs for the residual)
+  std::vector<double> h2f64; // double(h2f_i): rhs used by the residual (c16)
   T gl, gr;                  // Dirichlet values at x=0 and x=1
 };
 
@@ -149,7 +152,7 @@ struct Problem2D {
   int64_t nx, ny;
   double h2;
   std::vector<T> h2f;        // nx*ny, row-major
-  std::vector<double> h2f64; // nx*ny
+  std::vector<double> h2f64; // nx*ny, double(h2f) (c16)
   int64_t pitch() const { return nx + 2; }
 };
 
@@ -268,8 +271,8 @@ int solve1d(int64_t n, double h, const double* f, const double* bc, const double
   p.h2f.resize(n);
   p.h2f64.resize(n);
   for (int64_t i = 0; i < n; ++i) {
-    p.h2f64[i] = p.h2 * f[i];
-    p.h2f[i] = (T)p.h2f64[i];
+    p.h2f[i] = (T)(p.h2 * f[i]);
+    p.h2f64[i] = (double)p.h2f[i];  // reading c16: residual of the rounded system
   }
   std::vector<T> xa(n + 2), xb(n + 2);
   xa[0] = xb[0] = bc ? (T)bc[0] : T(0);
@@ -302,8 +305,8 @@ int solve2d(int64_t nx, int64_t ny, double h, const double* f, const double* bc,
   p.h2f.resize(nx * ny);
   p.h2f64.resize(nx * ny);
   for (int64_t q = 0; q < nx * ny; ++q) {
-    p.h2f64[q] = p.h2 * f[q];
-    p.h2f[q] = (T)p.h2f64[q];
+    p.h2f[q] = (T)(p.h2 * f[q]);
+    p.h2f64[q] = (double)p.h2f[q];  // reading c16: residual of the rounded system
   }
   std::vector<T> xa((nx + 2) * (ny + 2), T(0));
   // Dirichlet ring (reading c12): south row j=0, north row j=ny+1, west col i=0, east col i=nx+1
