@@ -1,0 +1,289 @@
+"""Benchmark of the hierarchical Jacobi hot path (BASELINE.json metric) — one JSON line.
+
+Workload (BASELINE.json configs[3], the configuration the "1/2/4/8 B200" metric is quoted on;
+it fits one GPU): 2D Poisson 16384^2, fp64, 32x32 tiles, k = 16 sub-iterations, the paper's
+protocol (f = 1, x0 = 1, g = 0).  One STEP = one cycle = the whole hot path
+(tile+halo load, fused residual of the snapshot, k sub-sweeps, interior store, residual
+reduction + stopping test).  value = cell-updates/s = nx*ny*k / (ms_per_step) summed over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (row slabs, NCCL halos + allreduce)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-to-residual-1e-6 and cell-updates/s (% HBM roofline) at 1/2/4/8 B200"
+N_GRID = 16384
+TILE = 32
+K_SUB = 16
+BYTES_PER_CELL = 24  # x_c read 8 + h2f read 8 + x_{c+1} write 8
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=6)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_GRID)
+    ap.add_argument("--k", type=int, default=K_SUB)
+    ap.add_argument("--mode", default="hier", choices=["hier", "classic"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "smem"])
+    ap.add_argument("--ttt", type=float, default=1e-4,
+                    help="also measure time-to-tolerance at this relative tol (0 = skip)")
+    ap.add_argument("--e2e-cycles", type=int, default=32)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def ncu_traffic():
+    """dram bytes per launch of the cycle kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_cycle_kernel.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("dram_bytes_per_launch")
+    return None
+
+
+def cpu_oracle_sample(n_cells_side, k, cycles):
+    """Time the CPU oracle (as it stands, single-threaded) on a bounded sample of the workload."""
+    import numpy as np
+    import oracle
+    from paper_2006_16465_b200.inputs import make_problem
+    p = make_problem("P", 2, n_cells_side)
+    oracle.build()
+    t0 = time.perf_counter()
+    oracle.solve(2, n_cells_side, n_cells_side, p["h"], p["f"], p["bc"], p["x0"], mode="hier",
+                 tile=(TILE, TILE), k=k, tol=0.0, max_cycles=cycles, history=False)
+    dt = time.perf_counter() - t0
+    return n_cells_side * n_cells_side * k * cycles / dt, dt
+
+
+def run_reference(args, rank):
+    """--impl reference: the CPU oracle (this tier's reference arm) on the host cores."""
+    if rank != 0:
+        return
+    side = 8192 if args.n >= 8192 else args.n
+    vals = []
+    for _ in range(max(1, min(args.steps, 2))):
+        v, dt = cpu_oracle_sample(side, args.k, 1)
+        vals.append(v)
+    v = sorted(vals)[len(vals) // 2]
+    sample = f"1 cycle of the same method (32x32 tiles, k={args.k}, paper protocol) on a {side}^2 grid per step"
+    out = {"metric": METRIC, "value": v, "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": len(vals),
+           "warmup": 0, "ms_per_step": side * side * args.k / v * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": f"2D Poisson {args.n}^2 fp64, 32x32 tiles, k={args.k} (sampled {side}^2)",
+                      "grid": args.n, "tile": [TILE, TILE], "k": args.k},
+           "cpu_baseline": {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "oracle", "sample": sample},
+           "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2006_16465_b200 import hj
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, k = args.n, (args.k if args.mode == "hier" else 1)
+    h = 1.0 / (n + 1)
+    # row slab of this rank (whole tile rows; PAPER-faithful tiles never straddle ranks)
+    unit = TILE if args.mode == "hier" else 16
+    rows_units = (n + unit - 1) // unit
+    rb = (rows_units * rank // world) * unit
+    re = min((rows_units * (rank + 1) // world) * unit, n)
+    nloc = re - rb
+    f = torch.ones(nloc * n, dtype=torch.float64, device=dev)     # protocol P
+    x0 = torch.ones(nloc * n, dtype=torch.float64, device=dev)
+    bc = torch.zeros(4 * n, dtype=torch.float64, device=dev)
+    prm = dict(mode=args.mode, tile=(TILE, TILE), k=k, tol=0.0, max_cycles=1 << 62, kernel=args.kernel)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    if world > 1:
+        idb = [hj.hj_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(idb, src=0)
+        plan = hj.DistPlan(n, n, h, f, bc, x0, rank=rank, nranks=world, nccl_id=idb[0], row_begin=rb,
+                           row_end=re, stream=stream, **prm)
+    else:
+        plan = hj.Plan(2, n, n, h, f, bc, x0, stream=stream, **prm)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (also instantiates graphs / events)
+    plan.run(args.warmup, timed=True)
+    barrier()
+    cells_local = nloc * n
+    with ClockSampler(local) as clk:
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        kernel_ms = plan.run(args.steps, timed=True)   # events around each cycle kernel, on its stream
+        e1.record()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms, kernel_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, kernel_ms = t.tolist()
+    ms_step = ms / args.steps
+    kern_ms = kernel_ms / args.steps
+    value = n * n * k / (ms_step * 1e-3)
+
+    # time to tolerance (paper protocol, measured) and projection to 1e-6
+    ttt = None
+    if args.ttt > 0 and world == 1:
+        plan.close()
+        tplan = hj.Plan(2, n, n, h, f, bc, x0, stream=stream, mode=args.mode, tile=(TILE, TILE), k=k,
+                        tol=args.ttt, max_cycles=10**7, kernel=args.kernel)
+        r = tplan.solve(history=False)
+        ttt = {"tol": args.ttt, "protocol": "P (f=1, x0=1, g=0)", "cycles": r["cycles"],
+               "converged": r["converged"], "seconds": r["seconds_solve"], "measured": True}
+        tplan.close()
+    else:
+        plan.close()
+
+    # end to end through the public C-ABI with host buffers (pinned), H2D/D2H inside
+    e2e = None
+    if world == 1:
+        fh = torch.ones(n * n, dtype=torch.float64).pin_memory()
+        xh = torch.ones(n * n, dtype=torch.float64).pin_memory()
+        bh = torch.zeros(4 * n, dtype=torch.float64).pin_memory()
+        C = args.e2e_cycles
+        vals = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            r = hj.jacobi_solve(2, n, n, h, fh.numpy(), bh.numpy(), xh.numpy(), history=False, mode=args.mode,
+                                tile=(TILE, TILE), k=k, tol=0.0, max_cycles=C, kernel=args.kernel)
+            vals.append(time.perf_counter() - t0)
+        sec = min(vals)
+        e2e = {"value": n * n * k * C / sec, "unit": "cell-updates/s",
+               "h2d_bytes_per_step": (2 * n * n + 4 * n) * 8 // C, "d2h_bytes_per_step": n * n * 8 // C,
+               "cycles_per_call": C, "api": "jacobi_solve (host buffers, pinned)", "seconds_per_call": sec}
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    peak, peak_src = measured_peaks()
+    achieved = BYTES_PER_CELL * n * n / world / (kern_ms * 1e-3) / 1e9   # per-GPU kernel GB/s
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        side = 8192
+        v, dt = cpu_oracle_sample(side, k, 1)
+        cpu = {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+               "sample": f"1 cycle of the same method on a {side}^2 grid (1/4 of the workload's cells; "
+                         f"identical per-cell work), {dt:.1f} s single-threaded"}
+    proj = None
+    if ttt is not None:
+        proj = {"tol": 1e-6, "cycles_model": 6.1e6, "seconds": 6.1e6 * ms_step * 1e-3, "measured": False,
+                "note": "projected: steady per-cycle time x model cycle count (SURVEY.md §8(d))"}
+    out = {"metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"cfg4: 2D Poisson {n}^2 fp64, {TILE}x{TILE} tiles, k={k}, mode={args.mode}, "
+                                  f"paper protocol f=1 x0=1", "grid": n, "tile": [TILE, TILE], "k": k,
+                      "mode": args.mode, "kernel": args.kernel, "parallelism": f"row-slab x{world}",
+                      "l2": "inputs 6.4 GB >> 126 MB L2, no flush needed"},
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "traffic": ncu_traffic(), "peak_source": peak_src,
+                        "kernel_ms": kern_ms, "bytes_per_cell": BYTES_PER_CELL},
+           "cpu_baseline": cpu,
+           "e2e": e2e,
+           "gpu_launches": args.steps * plan.launches_per_cycle_static,
+           "clocks": clk.summary(),
+           "time_to_tol": ttt,
+           "time_to_1e-6": proj}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

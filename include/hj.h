@@ -1,0 +1,161 @@
+/* include/hj.h — C-ABI of the B200-native hierarchical Jacobi solver (libhj.so).
+ *
+ * What it solves: the finite-difference Poisson problem of the paper
+ *   1D  -u'' = f on (0,1), 3-point stencil, A = tridiag(-1,2,-1)/h^2   PAPER.md:180-207 (§3.4, Eq. 5)
+ *   2D  -(u_xx+u_yy) = f, 5-point stencil, dx = dy = h                PAPER.md:393-421 (§4.2)
+ * with Dirichlet data g on the ring, by
+ *   HJ_CLASSIC       one global-memory Jacobi sweep per cycle          PAPER.md:114-133 (§3.2)
+ *   HJ_HIERARCHICAL  the paper's cycle: copy each tile + 1-cell halo on chip, k Jacobi
+ *                    sub-iterations with the halo frozen, write the interior back
+ *                                                                      PAPER.md:161-166 (§3.3),
+ *                                                                      :382-387 (§4.1), App. A :532-575
+ * until ||f - A x_c||_2 <= tol * ||f - A x_0||_2 (relative) or
+ * ||f - A x_c||_2 <= tol (absolute).  Readings of the paper: DESIGN.md §3.
+ *
+ * Conventions shared by every entry point
+ *  - Arrays are row-major with x fastest: f[j*nx + i], 0 <= i < nx, 0 <= j < ny.
+ *  - bc (Dirichlet ring): dim 1: [g_left, g_right]; dim 2: [south(nx) | north(nx) | west(ny) |
+ *    east(ny)], south = the row below j = 0.  NULL means g = 0 (the paper's u = 0).
+ *  - x0 NULL means a zero initial guess (the paper's protocol passes ones).
+ *  - Iterates are kept in hj_params.dtype (f64 or f32); the residual is always accumulated in
+ *    f64 from s = h^2 f - (stencil applied to x) (h^2-scaled form, reported unscaled).
+ *  - Ownership: every input pointer is borrowed for the duration of the call only; every
+ *    output buffer is caller-allocated; the library allocates and frees its own device
+ *    scratch (two padded iterate buffers, the h^2 f array, residual partials, history).
+ *  - Errors: a non-OK status leaves a message in hj_last_error() (thread-local).  Invalid
+ *    arguments/configurations are detected before any device work.  Not converging within
+ *    max_cycles is NOT an error (HJ_NOT_CONVERGED, outputs valid).  A non-finite residual
+ *    stops the solve with HJ_ERR_NUMERIC; outputs then hold the iterate whose residual was
+ *    non-finite and the history up to it.
+ *  - Thread-compatibility: one call per plan at a time; distinct plans may run concurrently.
+ *  - There is no CPU fallback: without a usable sm_100 device every call returns HJ_ERR_CUDA.
+ */
+#ifndef HJ_H_
+#define HJ_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HJ_OK = 0,
+  HJ_NOT_CONVERGED = 1,      /* outputs valid, cycles == max_cycles                           */
+  HJ_ERR_INVALID_ARG = 2,    /* NULL pointer, dim not 1/2, n < 1, h <= 0 or non-finite, ...    */
+  HJ_ERR_INVALID_CONFIG = 3, /* tile < 1 or > n, k < 1 (classic: k != 1), overlap != 0,
+                                tol < 0 / >= 1 (relative) / NaN, max_cycles < 0, tile does not
+                                fit on chip, slab rows not a multiple of tile_y              */
+  HJ_ERR_NUMERIC = 4,        /* NaN/Inf residual                                               */
+  HJ_ERR_CUDA = 5,
+  HJ_ERR_NCCL = 6,
+  HJ_ERR_OOM = 7
+} hj_status;
+
+typedef enum { HJ_F64 = 0, HJ_F32 = 1 } hj_dtype;
+typedef enum { HJ_HIERARCHICAL = 0, HJ_CLASSIC = 1 } hj_mode;
+typedef enum { HJ_TOL_RELATIVE = 0, HJ_TOL_ABSOLUTE = 1 } hj_tol_mode;
+typedef enum {
+  HJ_KERNEL_AUTO = 0,   /* register-resident warp-per-tile kernel where the tile shape allows
+                           (2D 32x32; 1D tile = 32*2^m <= 1024), else the shared-memory kernel */
+  HJ_KERNEL_SMEM = 1    /* the paper's design: one CTA per tile, one thread per DOF, shared-
+                           memory ping-pong with __syncthreads between sub-iterations          */
+} hj_kernel;
+
+typedef struct {
+  int32_t dim;           /* 1 or 2                                                           */
+  int64_t nx, ny;        /* interior points per direction; dim 1 => ny == 1                  */
+  double h;              /* grid spacing (hx == hy == h)                                      */
+  const double *f;       /* nx*ny right-hand side of -Δu = f (the paper's b)                  */
+  const double *bc;      /* ring values (layout above) or NULL                               */
+  const double *x0;      /* nx*ny initial guess or NULL                                       */
+} hj_problem;
+
+typedef struct {
+  hj_mode mode;
+  hj_dtype dtype;
+  int32_t tile_x, tile_y;  /* subdomain interior (the paper's blockDim.x/.y); dim 1: tile_y=1 */
+  int32_t k;               /* sub-iterations per cycle (>= 1; classic: 1)                    */
+  int32_t overlap;         /* must be 0 in this version (overlapping subdomains: next)       */
+  double tol;
+  hj_tol_mode tol_mode;
+  double ref_residual;     /* 0: r_0 = ||f - A x0||; > 0: use this r_0 (resume a solve)      */
+  int64_t max_cycles;      /* >= 0                                                            */
+  hj_kernel kernel;        /* kernel family selection (HJ_KERNEL_AUTO recommended)           */
+} hj_params;
+
+typedef struct {
+  double *x;               /* caller-allocated nx*ny doubles (f64 even for f32 solves)       */
+  double *history;         /* caller-allocated max_cycles+1 doubles or NULL;
+                              history[c] = ||f - A x_c||_2 for c = 0..cycles                  */
+  int64_t cycles;          /* first c at which the test held (0 if x0 already satisfies it)  */
+  int32_t converged;
+  double initial_residual; /* ||f - A x0||_2                                                  */
+  double final_residual;   /* ||f - A x_cycles||_2                                            */
+  double seconds_solve;    /* cycle loop only (device-resident data)                          */
+  double seconds_total;    /* whole call, incl. allocation and H2D/D2H copies (paper style)  */
+} hj_result;
+
+/* Host pointers in problem and result.  Blocking. */
+hj_status jacobi_solve(const hj_problem *problem, const hj_params *params, hj_result *result);
+
+/* Device pointers in problem (f, bc, x0) and result (x, history); cuda_stream is a
+ * cudaStream_t (NULL = the legacy default stream).  Returns when the solve is complete. */
+hj_status jacobi_solve_device(const hj_problem *problem, const hj_params *params,
+                              hj_result *result, void *cuda_stream);
+
+/* ---- plans: set up once (device pointers), run cycles many times (benchmarks, resume) ---- */
+typedef struct hj_plan hj_plan;
+
+/* Allocates the padded iterate buffers, h^2 f and scratch on the current device and
+ * initialises them from problem (device pointers; copied, not retained). */
+hj_status hj_plan_create(const hj_problem *problem, const hj_params *params, void *cuda_stream,
+                         hj_plan **plan);
+/* Re-initialise the iterate to the problem's x0 (kept in a device copy) and the cycle count to 0. */
+hj_status hj_plan_reset(hj_plan *plan);
+/* Launch exactly ncycles cycles from the current state without host synchronisation; each
+ * cycle = the cycle kernel + residual reduction (one "step").  If kernel_ms is not NULL, CUDA
+ * events on the plan's stream bracket every cycle-kernel launch and *kernel_ms receives the
+ * sum of their durations (the call then synchronises once, at the end). */
+hj_status hj_plan_run(hj_plan *plan, int64_t ncycles, float *kernel_ms);
+/* Run to convergence (or max_cycles) from the current state and fill result
+ * (x and history are DEVICE pointers or NULL). */
+hj_status hj_plan_solve(hj_plan *plan, hj_result *result);
+/* Number of launches of library kernels per cycle (for launch accounting). */
+int32_t hj_plan_launches_per_cycle(const hj_plan *plan);
+hj_status hj_plan_destroy(hj_plan *plan);
+
+/* ---- multi-GPU: row slabs, one process per GPU (PAPER.md has no multi-GPU; north star) ---- */
+typedef struct {
+  int32_t rank, nranks;
+  const char *nccl_id;     /* 128 bytes from hj_nccl_unique_id() on rank 0, broadcast by caller */
+  int64_t row_begin, row_end; /* this rank's interior rows [begin, end) of the global grid;
+                                 multiples of tile_y (hierarchical) / of 16 (classic)        */
+} hj_dist;
+
+hj_status hj_nccl_unique_id(char out[128]);
+/* Plan for one rank of a row-slab solve: problem->f and ->x0 are DEVICE pointers to the local
+ * rows [row_begin, row_end), problem->bc a DEVICE pointer to the full ring (or NULL).  Creating
+ * the plan initialises NCCL (collective over all ranks) and exchanges the initial halos. */
+hj_status hj_plan_create_dist(const hj_problem *problem, const hj_params *params,
+                              const hj_dist *dist, void *cuda_stream, hj_plan **plan);
+/* problem: GLOBAL nx, ny, h and bc (host pointers, full ring); f and x0 hold ONLY the local
+ * rows [row_begin, row_end) (host pointers).  result->x receives the local rows; history is
+ * global (identical on every rank).  Cycle counts and iterates are bitwise identical to the
+ * single-GPU solve for any nranks (tile rows never straddle slabs). */
+hj_status jacobi_solve_dist(const hj_problem *problem, const hj_params *params,
+                            hj_result *result, const hj_dist *dist);
+
+/* Resource figures of the paper (o = 0): tiles = the paper's block count,
+ * threads = tiles*tile_x*tile_y, smem_bytes_paper_formula = sizeof(T)*(2(Tx+2)+Tx) in 1D
+ * and sizeof(T)*(2(Tx+2)(Ty+2)+TxTy) in 2D. Host-only. */
+hj_status hj_resource_figures(const hj_problem *problem, const hj_params *params,
+                              int64_t *tiles, int64_t *threads, int64_t *smem_bytes_paper_formula);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char *hj_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HJ_H_ */

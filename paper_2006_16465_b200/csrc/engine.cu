@@ -1,0 +1,739 @@
+// Host engine and C-ABI of libhj.so (include/hj.h).
+//
+// A plan owns: two padded iterate buffers X[0], X[1] (snapshot semantics, DESIGN.md §3 c6),
+// H2F = T(h^2 f), per-tile residual partials, per-row-group sums, the residual history and a
+// device control block.  One cycle = cycle kernel (reads X[p], writes X[p^1], reduces the
+// residual of X[p]) -> rowsum -> finalize (history, stopping test).  The stopping test runs on
+// the device; cycles after convergence are no-ops, so the host captures G cycles in a CUDA
+// graph and polls the control block once per graph launch.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "hj_internal.cuh"
+#include "hj_plan.h"
+
+namespace hj {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+cudaError_t configure_2d();
+cudaError_t configure_1d();
+
+namespace {
+
+// ------------------------------------------------------------------ kernels --
+
+// Fill a padded iterate buffer: ring from bc, interior from x0 (or zero), pads zero.
+// dist: rows [0, R+1] of the slab; global row of local row r is gy0 + r (0 = south ring).
+template <typename T>
+__global__ void init_x_kernel(T* __restrict__ X, long long pitch, long long rows, int dim, long long nx,
+                              long long ny_global, long long gy0, long long ny_local,
+                              const double* __restrict__ bc, const double* __restrict__ x0,
+                              int with_interior, int col0) {
+  const long long n = pitch * rows;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long r = q / pitch, cc = q % pitch;
+    const long long i = cc - (col0 - 1);  // padded x index: 0 = west ring, nx+1 = east ring
+    T v = T(0);
+    if (dim == 1) {
+      if (i == 0) v = bc ? (T)bc[0] : T(0);
+      else if (i == nx + 1) v = bc ? (T)bc[1] : T(0);
+      else if (i >= 1 && i <= nx && with_interior && x0) v = (T)x0[i - 1];
+    } else if (i >= 0 && i <= nx + 1 && r <= ny_local + 1) {
+      const long long gj = gy0 + r;  // global padded row
+      const bool iin = i >= 1 && i <= nx;
+      if (gj == 0) {
+        if (iin && bc) v = (T)bc[i - 1];
+      } else if (gj == ny_global + 1) {
+        if (iin && bc) v = (T)bc[nx + i - 1];
+      } else if (r >= 1 && r <= ny_local) {
+        if (i == 0) v = bc ? (T)bc[2 * nx + gj - 1] : T(0);
+        else if (i == nx + 1) v = bc ? (T)bc[2 * nx + ny_global + gj - 1] : T(0);
+        else if (with_interior && x0) v = (T)x0[(r - 1) * nx + (i - 1)];
+      }
+    }
+    X[q] = v;
+  }
+}
+
+template <typename T>
+__global__ void init_h2f_kernel(T* __restrict__ H, long long fpitch, long long frows, long long nx,
+                                long long ny, const double* __restrict__ f, double h2) {
+  const long long n = fpitch * frows;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long j = q / fpitch, i = q % fpitch;
+    H[q] = (i < nx && j < ny) ? (T)(h2 * f[j * nx + i]) : T(0);
+  }
+}
+
+// Extract the interior of X into a dense double array (row-major).
+template <typename T>
+__global__ void extract_kernel(const T* __restrict__ X, long long pitch, int dim, long long nx,
+                               long long ny, int col0, double* __restrict__ out) {
+  const long long n = nx * ny;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long j = q / nx, i = q % nx;
+    out[q] = (double)X[(dim == 1 ? 0 : (j + 1) * pitch) + col0 + i];
+  }
+}
+
+// R[rg_offset + g] = sum_{p < ppr} part[g*ppr + p], fixed order (lane-strided, then an xor tree).
+__global__ void rowsum_kernel(const double* __restrict__ part, long long ppr, long long nrg,
+                              long long rg_offset, double* __restrict__ R, const Ctrl* __restrict__ ctrl) {
+  if (ctrl->done) return;
+  const long long g = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g >= nrg) return;
+  double s = 0.0;
+  for (long long p = lane; p < ppr; p += 32) s += part[g * ppr + p];
+  s = warp_sum(s);
+  if (lane == 0) R[rg_offset + g] = s;
+}
+
+// S_c = sum of R (fixed order); history; the stopping test of DESIGN.md §3 (c1, c14):
+// c = 0: converged iff S_0 == 0 (or the test holds with an explicit r_0 / absolute mode);
+// c >= 1: converged iff sqrt(S_c) <= tol * sqrt(S_0)  (absolute: sqrt(S_c)/h^2 <= tol).
+__global__ void finalize_kernel(const double* __restrict__ R, long long nrg, Ctrl* __restrict__ ctrl,
+                                double* __restrict__ hist, long long hist_cap, double h2, double tol,
+                                int tol_mode, double ref_residual, long long max_cycles) {
+  if (ctrl->done) return;
+  __shared__ double ws[32];
+  double s = 0.0;
+  for (long long p = threadIdx.x; p < nrg; p += blockDim.x) s += R[p];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double S = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) S += ws[w];
+  const long long c = ctrl->c;
+  if (hist && c < hist_cap) hist[c] = sqrt(S) / h2;
+  ctrl->S_last = S;
+  if (c == 0) {
+    ctrl->S0 = S;
+    ctrl->sqrtS0 = ref_residual > 0.0 ? ref_residual * h2 : sqrt(S);
+  }
+  bool conv;
+  if (!isfinite(S)) {
+    ctrl->status = HJ_ERR_NUMERIC;
+    ctrl->done = 1;
+    ctrl->c_done = c;
+    return;
+  }
+  const double sq = sqrt(S);
+  const bool test = tol_mode == 0 ? (sq <= tol * ctrl->sqrtS0) : (sq / h2 <= tol);
+  if (c == 0) conv = (S == 0.0) || ((ref_residual > 0.0 || tol_mode == 1) && test);
+  else conv = test;
+  if (conv) {
+    ctrl->done = 1;
+    ctrl->converged = 1;
+    ctrl->status = HJ_OK;
+    ctrl->c_done = c;
+  } else if (c >= max_cycles) {
+    ctrl->done = 1;
+    ctrl->converged = 0;
+    ctrl->status = HJ_NOT_CONVERGED;
+    ctrl->c_done = c;
+  } else {
+    ctrl->c = c + 1;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+hj_status make_tmap(CUtensorMap* tm, const void* base, int dtype, uint64_t d0, uint64_t d1,
+                    uint64_t stride_bytes, uint32_t b0, uint32_t b1) {
+  auto enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return HJ_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {d0, d1};
+  cuuint64_t strides[1] = {stride_bytes};
+  cuuint32_t box[2] = {b0, b1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(tm, dtype == HJ_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                   2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return HJ_ERR_CUDA;
+  }
+  return HJ_OK;
+}
+
+long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
+
+hj_status ensure_configured(int* nsm) {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  static int sms = 0;
+  std::call_once(once, [] {
+    int dev = 0;
+    err = cudaGetDevice(&dev);
+    if (err == cudaSuccess) {
+      cudaDeviceProp prop;
+      err = cudaGetDeviceProperties(&prop, dev);
+      if (err == cudaSuccess && prop.major < 10) err = cudaErrorInvalidDevice;
+      sms = prop.multiProcessorCount;
+    }
+    if (err == cudaSuccess) err = configure_2d();
+    if (err == cudaSuccess) err = configure_1d();
+  });
+  if (err != cudaSuccess) {
+    set_error(std::string("libhj: no usable sm_100 device: ") + cudaGetErrorString(err));
+    return HJ_ERR_CUDA;
+  }
+  *nsm = sms;
+  return HJ_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- validation ---
+hj_status validate(const hj_problem* pb, const hj_params* pr, bool need_f) {
+  if (!pb || !pr) { set_error("NULL problem or params"); return HJ_ERR_INVALID_ARG; }
+  if (pb->dim != 1 && pb->dim != 2) { set_error("dim must be 1 or 2"); return HJ_ERR_INVALID_ARG; }
+  if (pb->nx < 1 || pb->ny < 1 || (pb->dim == 1 && pb->ny != 1)) {
+    set_error("nx, ny must be >= 1 (dim 1: ny == 1)");
+    return HJ_ERR_INVALID_ARG;
+  }
+  if (!(pb->h > 0.0) || !std::isfinite(pb->h)) { set_error("h must be finite and > 0"); return HJ_ERR_INVALID_ARG; }
+  if (need_f && !pb->f) { set_error("f is NULL"); return HJ_ERR_INVALID_ARG; }
+  if (pb->nx > (1LL << 30) || pb->ny > (1LL << 30)) { set_error("grid too large"); return HJ_ERR_INVALID_ARG; }
+  if (pr->mode != HJ_HIERARCHICAL && pr->mode != HJ_CLASSIC) { set_error("bad mode"); return HJ_ERR_INVALID_CONFIG; }
+  if (pr->dtype != HJ_F64 && pr->dtype != HJ_F32) { set_error("bad dtype"); return HJ_ERR_INVALID_CONFIG; }
+  if (pr->overlap != 0) { set_error("overlap must be 0 in this version"); return HJ_ERR_INVALID_CONFIG; }
+  if (std::isnan(pr->tol) || pr->tol < 0.0 || (pr->tol_mode == HJ_TOL_RELATIVE && pr->tol >= 1.0)) {
+    set_error("tol must be in [0, 1) (relative) or >= 0 (absolute)");
+    return HJ_ERR_INVALID_CONFIG;
+  }
+  if (pr->tol_mode != HJ_TOL_RELATIVE && pr->tol_mode != HJ_TOL_ABSOLUTE) { set_error("bad tol_mode"); return HJ_ERR_INVALID_CONFIG; }
+  if (pr->max_cycles < 0) { set_error("max_cycles must be >= 0"); return HJ_ERR_INVALID_CONFIG; }
+  if (!(pr->ref_residual >= 0.0) || !std::isfinite(pr->ref_residual)) { set_error("bad ref_residual"); return HJ_ERR_INVALID_CONFIG; }
+  if (pr->kernel != HJ_KERNEL_AUTO && pr->kernel != HJ_KERNEL_SMEM) { set_error("bad kernel"); return HJ_ERR_INVALID_CONFIG; }
+  if (pr->mode == HJ_CLASSIC) {
+    if (pr->k != 1) { set_error("classic mode needs k == 1"); return HJ_ERR_INVALID_CONFIG; }
+    return HJ_OK;
+  }
+  if (pr->k < 1) { set_error("k must be >= 1"); return HJ_ERR_INVALID_CONFIG; }
+  if (pr->tile_x < 1 || pr->tile_x > pb->nx) { set_error("tile_x must be in [1, nx]"); return HJ_ERR_INVALID_CONFIG; }
+  if (pb->dim == 1 && pr->tile_y != 1) { set_error("dim 1 needs tile_y == 1"); return HJ_ERR_INVALID_CONFIG; }
+  if (pb->dim == 2 && (pr->tile_y < 1 || pr->tile_y > pb->ny)) { set_error("tile_y must be in [1, ny]"); return HJ_ERR_INVALID_CONFIG; }
+  return HJ_OK;
+}
+
+// Choose the kernel and check it can run the tile shape.
+static hj_status choose_kernel(const hj_problem* pb, const hj_params* pr, int* kind) {
+  const size_t esz = pr->dtype == HJ_F64 ? 8 : 4;
+  if (pr->mode == HJ_CLASSIC) { *kind = pb->dim == 2 ? K_CLASSIC2D : K_CLASSIC1D; return HJ_OK; }
+  if (pb->dim == 2) {
+    if (pr->kernel == HJ_KERNEL_AUTO && pr->tile_x == 32 && pr->tile_y == 32) { *kind = K_REG2D; return HJ_OK; }
+    const size_t smem = esz * (2 * size_t(pr->tile_x + 2) * (pr->tile_y + 2) + size_t(pr->tile_x) * pr->tile_y);
+    if ((long long)pr->tile_x * pr->tile_y > 1024 || smem > 200 * 1024) {
+      set_error("tile does not fit one CTA (tile_x*tile_y <= 1024 and paper smem <= 200 KiB)");
+      return HJ_ERR_INVALID_CONFIG;
+    }
+    *kind = K_SMEM2D;
+    return HJ_OK;
+  }
+  const int t = pr->tile_x;
+  if (pr->kernel == HJ_KERNEL_AUTO && t % 32 == 0 && t <= 1024 && ((t / 32) & (t / 32 - 1)) == 0) {
+    *kind = K_REG1D;
+    return HJ_OK;
+  }
+  if (t > 1024) { set_error("1D tile must be <= 1024"); return HJ_ERR_INVALID_CONFIG; }
+  *kind = K_SMEM1D;
+  return HJ_OK;
+}
+
+// ------------------------------------------------------------------ plans ---
+hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st, const DistInfo* di,
+                     hj_plan** out) {
+  HJ_TRY(validate(pb, pr, true));
+  int nsm = 0;
+  HJ_TRY(ensure_configured(&nsm));
+  hj_plan* P = new hj_plan();
+  P->prm = *pr;
+  Geom& g = P->g;
+  g.dim = pb->dim;
+  g.dtype = pr->dtype;
+  g.mode = pr->mode;
+  g.h = pb->h;
+  g.h2 = pb->h * pb->h;
+  g.nx = pb->nx;
+  const long long ny_global = pb->ny;
+  g.ny = di ? (di->row_end - di->row_begin) : pb->ny;
+  g.tx = pr->mode == HJ_CLASSIC ? 1 : pr->tile_x;
+  g.ty = pr->mode == HJ_CLASSIC ? 1 : pr->tile_y;
+  g.k = pr->mode == HJ_CLASSIC ? 1 : pr->k;
+  hj_status s = choose_kernel(pb, pr, &g.kernel_kind);
+  if (s != HJ_OK) { delete P; return s; }
+  P->nsm = nsm;
+  const size_t esz = pr->dtype == HJ_F64 ? 8 : 4;
+  g.col0 = 16 / esz;
+  // tiles / partial layout
+  const long long gy0 = di ? di->row_begin : 0;
+  switch (g.kernel_kind) {
+    case K_REG2D: case K_SMEM2D:
+      g.ntx = (g.nx + g.tx - 1) / g.tx;
+      g.nty = (g.ny + g.ty - 1) / g.ty;
+      g.nrg_global = (ny_global + g.ty - 1) / g.ty;
+      g.rg_offset = gy0 / g.ty;
+      break;
+    case K_CLASSIC2D:
+      g.ntx = (g.nx + CLASSIC2D_COLS - 1) / CLASSIC2D_COLS;
+      g.nty = (g.ny + CLASSIC2D_ROWS - 1) / CLASSIC2D_ROWS;
+      g.nrg_global = (ny_global + CLASSIC2D_ROWS - 1) / CLASSIC2D_ROWS;
+      g.rg_offset = gy0 / CLASSIC2D_ROWS;
+      break;
+    case K_REG1D: case K_SMEM1D:
+      g.ntx = (g.nx + g.tx - 1) / g.tx; g.nty = 1; g.nrg_global = 1; g.rg_offset = 0;
+      break;
+    default:
+      g.ntx = (g.nx + CLASSIC1D_CELLS - 1) / CLASSIC1D_CELLS; g.nty = 1; g.nrg_global = 1; g.rg_offset = 0;
+  }
+  g.ntiles = g.ntx * g.nty;
+  g.parts_per_row = g.ntx;
+  g.nrg_local = g.nty;
+  // buffer geometry
+  if (g.dim == 2) {
+    g.pitch = round_up(g.nx + 2 * g.col0 + 2, 256 / esz);  // 256-B rows
+    g.rows = g.ny + 2;
+    g.fpitch = round_up(g.nx, 128 / esz);
+    g.frows = g.ny;
+  } else {
+    const long long span = g.ntx * (long long)(g.kernel_kind == K_CLASSIC1D ? CLASSIC1D_CELLS : g.tx);
+    g.pitch = round_up(span + 4 * g.col0 + 64, 256 / esz);
+    g.rows = 1;
+    g.fpitch = round_up(span + 64, 128 / esz);
+    g.frows = 1;
+  }
+  P->stream = st;
+  P->ny_global = ny_global;
+  P->gy0 = gy0;
+  P->hist_cap = pr->max_cycles + 1 < HIST_CAP ? pr->max_cycles + 1 : HIST_CAP;
+  const size_t xbytes = size_t(g.pitch) * g.rows * esz;
+  const size_t fbytes = size_t(g.fpitch) * g.frows * esz;
+  auto fail = [&](hj_status e) { plan_free(P); return e; };
+#define PCK(call)                                                                          \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      set_error(std::string(#call) + ": " + cudaGetErrorString(e_));                      \
+      return fail(e_ == cudaErrorMemoryAllocation ? HJ_ERR_OOM : HJ_ERR_CUDA);             \
+    }                                                                                      \
+  } while (0)
+  PCK(cudaMalloc(&P->X[0], xbytes));
+  PCK(cudaMalloc(&P->X[1], xbytes));
+  PCK(cudaMalloc(&P->H2F, fbytes));
+  PCK(cudaMalloc(&P->part, sizeof(double) * (g.ntiles + 1)));
+  PCK(cudaMalloc(&P->rowpart, sizeof(double) * (g.nrg_global + 1)));
+  P->rowsum_dst = P->rowpart;
+  if (di) {
+    PCK(cudaMalloc(&P->rowpart_local, sizeof(double) * (g.nrg_global + 1)));
+    PCK(cudaMemsetAsync(P->rowpart_local, 0, sizeof(double) * (g.nrg_global + 1), st));
+    P->rowsum_dst = P->rowpart_local;
+    s = dist_create(P, di);
+    if (s != HJ_OK) return fail(s);
+  }
+  PCK(cudaMalloc(&P->hist, sizeof(double) * P->hist_cap));
+  PCK(cudaMalloc(&P->ctrl, sizeof(Ctrl)));
+  PCK(cudaMallocHost(&P->ctrl_h, sizeof(Ctrl)));
+  PCK(cudaEventCreate(&P->ev0));
+  PCK(cudaEventCreate(&P->ev1));
+  // keep device copies of x0 / bc so that hj_plan_reset can re-initialise
+  const long long nloc = g.nx * g.ny;
+  const long long nbc = g.dim == 1 ? 2 : 2 * g.nx + 2 * ny_global;
+  PCK(cudaMalloc(&P->bc_d, sizeof(double) * nbc));
+  if (pb->bc) PCK(cudaMemcpyAsync(P->bc_d, pb->bc, sizeof(double) * nbc, cudaMemcpyDefault, st));
+  else PCK(cudaMemsetAsync(P->bc_d, 0, sizeof(double) * nbc, st));
+  PCK(cudaMalloc(&P->x0_d, sizeof(double) * nloc));
+  if (pb->x0) PCK(cudaMemcpyAsync(P->x0_d, pb->x0, sizeof(double) * nloc, cudaMemcpyDefault, st));
+  else PCK(cudaMemsetAsync(P->x0_d, 0, sizeof(double) * nloc, st));
+  PCK(cudaMemsetAsync(P->rowpart, 0, sizeof(double) * (g.nrg_global + 1), st));
+  PCK(cudaMemsetAsync(P->part, 0, sizeof(double) * (g.ntiles + 1), st));
+  {
+    const int blocks = 4 * nsm;
+    if (esz == 8)
+      init_h2f_kernel<double><<<blocks, 256, 0, st>>>((double*)P->H2F, g.fpitch, g.frows, g.nx, g.ny, pb->f, g.h2);
+    else
+      init_h2f_kernel<float><<<blocks, 256, 0, st>>>((float*)P->H2F, g.fpitch, g.frows, g.nx, g.ny, pb->f, g.h2);
+    PCK(cudaGetLastError());
+  }
+  if (g.kernel_kind == K_REG2D) {
+    using u64 = uint64_t;
+    const uint32_t bw = (uint32_t)((((g.col0 + 33) * esz + 15) / 16) * 16 / esz);
+    for (int b = 0; b < 2; ++b) {
+      s = make_tmap(&P->tmX[b], P->X[b], g.dtype, (u64)g.pitch, (u64)g.rows, (u64)g.pitch * esz, bw, 34);
+      if (s != HJ_OK) return fail(s);
+    }
+    s = make_tmap(&P->tmF, P->H2F, g.dtype, (u64)g.fpitch, (u64)g.frows, (u64)g.fpitch * esz, 32, 32);
+    if (s != HJ_OK) return fail(s);
+  }
+  s = plan_reset(P);
+  if (s != HJ_OK) return fail(s);
+#undef PCK
+  *out = P;
+  return HJ_OK;
+}
+
+hj_status plan_reset(hj_plan* P) {
+  const Geom& g = P->g;
+  cudaStream_t st = P->stream;
+  const int blocks = 4 * P->nsm;
+  for (int b = 0; b < 2; ++b) {
+    if (g.dtype == HJ_F64)
+      init_x_kernel<double><<<blocks, 256, 0, st>>>((double*)P->X[b], g.pitch, g.rows, g.dim, g.nx,
+                                                     P->ny_global, P->gy0, g.ny, P->bc_d, P->x0_d,
+                                                     b == 0, (int)g.col0);
+    else
+      init_x_kernel<float><<<blocks, 256, 0, st>>>((float*)P->X[b], g.pitch, g.rows, g.dim, g.nx,
+                                                    P->ny_global, P->gy0, g.ny, P->bc_d, P->x0_d,
+                                                    b == 0, (int)g.col0);
+    HJ_CUDA(cudaGetLastError());
+  }
+  Ctrl c0;
+  std::memset(&c0, 0, sizeof(c0));
+  *P->ctrl_h = c0;
+  HJ_CUDA(cudaMemcpyAsync(P->ctrl, P->ctrl_h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+  if (P->dist) HJ_TRY(dist_initial_exchange(P));
+  HJ_CUDA(cudaStreamSynchronize(st));
+  P->c_host = 0;
+  return HJ_OK;
+}
+
+int launches_per_cycle(const hj_plan* P) { return P->dist ? 3 : 3; }
+
+// One cycle with static parity p: X[p] -> X[p^1].
+hj_status launch_cycle(hj_plan* P, int p, bool timed, float* acc_ms) {
+  const Geom& g = P->g;
+  cudaStream_t st = P->stream;
+  CycleArgs a;
+  a.xin = P->X[p];
+  a.xout = P->X[p ^ 1];
+  a.h2f = P->H2F;
+  a.tm_in = &P->tmX[p];
+  a.tm_f = &P->tmF;
+  a.part = P->part;
+  a.ctrl = P->ctrl;
+  a.max_cycles = P->prm.max_cycles;
+  (void)acc_ms;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timed) {
+    while (P->evpool.size() < 2 * (P->evused + 1)) {
+      cudaEvent_t ev;
+      HJ_CUDA(cudaEventCreate(&ev));
+      P->evpool.push_back(ev);
+    }
+    e0 = P->evpool[2 * P->evused];
+    e1 = P->evpool[2 * P->evused + 1];
+    P->evused++;
+    HJ_CUDA(cudaEventRecord(e0, st));
+  }
+  cudaError_t e = g.dim == 2 ? launch_cycle_2d(g, a, P->nsm, st) : launch_cycle_1d(g, a, P->nsm, st);
+  if (e != cudaSuccess) {
+    set_error(std::string("cycle kernel launch: ") + cudaGetErrorString(e));
+    return HJ_ERR_CUDA;
+  }
+  if (timed) HJ_CUDA(cudaEventRecord(e1, st));
+  if (P->dist) HJ_TRY(dist_halo_exchange(P, p ^ 1));
+  const int wpb = 8;
+  rowsum_kernel<<<(unsigned)((g.nrg_local + wpb - 1) / wpb), 32 * wpb, 0, st>>>(
+      P->part, g.parts_per_row, g.nrg_local, g.rg_offset, P->rowsum_dst, P->ctrl);
+  HJ_CUDA(cudaGetLastError());
+  if (P->dist) HJ_TRY(dist_allreduce(P));
+  finalize_kernel<<<1, 1024, 0, st>>>(P->rowpart, g.nrg_global, P->ctrl, P->hist, P->hist_cap, g.h2,
+                                      P->prm.tol, (int)P->prm.tol_mode, P->prm.ref_residual,
+                                      P->prm.max_cycles);
+  HJ_CUDA(cudaGetLastError());
+  return HJ_OK;
+}
+
+static hj_status drain_events(hj_plan* P, float* acc) {
+  if (P->evused == 0) return HJ_OK;
+  HJ_CUDA(cudaEventSynchronize(P->evpool[2 * P->evused - 1]));
+  for (int i = 0; i < P->evused; ++i) {
+    float ms = 0.f;
+    HJ_CUDA(cudaEventElapsedTime(&ms, P->evpool[2 * i], P->evpool[2 * i + 1]));
+    *acc += ms;
+  }
+  P->evused = 0;
+  return HJ_OK;
+}
+
+static hj_status get_graph(hj_plan* P, int G, cudaGraphExec_t* out) {
+  auto it = P->graphs.find(G);
+  if (it != P->graphs.end()) { *out = it->second; return HJ_OK; }
+  cudaGraph_t graph;
+  HJ_CUDA(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
+  hj_status s = HJ_OK;
+  for (int i = 0; i < G && s == HJ_OK; ++i) s = launch_cycle(P, i & 1, false, nullptr);
+  cudaError_t e = cudaStreamEndCapture(P->stream, &graph);
+  if (s != HJ_OK) return s;
+  if (e != cudaSuccess) { set_error(std::string("graph capture: ") + cudaGetErrorString(e)); return HJ_ERR_CUDA; }
+  cudaGraphExec_t ex;
+  e = cudaGraphInstantiate(&ex, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) { set_error(std::string("graph instantiate: ") + cudaGetErrorString(e)); return HJ_ERR_CUDA; }
+  P->graphs[G] = ex;
+  *out = ex;
+  return HJ_OK;
+}
+
+hj_status plan_run(hj_plan* P, long long ncycles, float* kernel_ms) {
+  if (ncycles < 0) { set_error("ncycles must be >= 0"); return HJ_ERR_INVALID_ARG; }
+  if (kernel_ms) {
+    // eager launches, CUDA events around every cycle kernel, one synchronisation at the end
+    *kernel_ms = 0.f;
+    P->evused = 0;
+    for (long long i = 0; i < ncycles; ++i) {
+      HJ_TRY(launch_cycle(P, (int)(P->c_host & 1), true, kernel_ms));
+      P->c_host++;
+      if (P->evused == 4096) HJ_TRY(drain_events(P, kernel_ms));
+    }
+    HJ_TRY(drain_events(P, kernel_ms));
+    return HJ_OK;
+  }
+  long long left = ncycles;
+  if (left > 0 && (P->c_host & 1)) {  // graphs start at even parity
+    HJ_TRY(launch_cycle(P, 1, false, nullptr));
+    P->c_host++;
+    left--;
+  }
+  while (left >= 2) {
+    const int G = left >= 64 ? 64 : (int)(left & ~1LL);
+    cudaGraphExec_t ex;
+    HJ_TRY(get_graph(P, G, &ex));
+    HJ_CUDA(cudaGraphLaunch(ex, P->stream));
+    P->c_host += G;
+    left -= G;
+  }
+  if (left == 1) {
+    HJ_TRY(launch_cycle(P, 0, false, nullptr));
+    P->c_host++;
+  }
+  return HJ_OK;
+}
+
+hj_status plan_solve(hj_plan* P, hj_result* res, double* x_dev, double* hist_dev) {
+  const Geom& g = P->g;
+  cudaStream_t st = P->stream;
+  HJ_CUDA(cudaEventRecord(P->ev0, st));
+  if (P->c_host & 1) {  // graphs start at even parity
+    HJ_TRY(launch_cycle(P, 1, false, nullptr));
+    P->c_host++;
+  }
+  int G = 2;
+  for (;;) {
+    cudaGraphExec_t ex;
+    HJ_TRY(get_graph(P, G, &ex));
+    HJ_CUDA(cudaGraphLaunch(ex, st));
+    P->c_host += G;
+    HJ_CUDA(cudaMemcpyAsync(P->ctrl_h, P->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    HJ_CUDA(cudaStreamSynchronize(st));
+    if (P->ctrl_h->done) break;
+    if (G < 256) G *= 2;
+  }
+  HJ_CUDA(cudaEventRecord(P->ev1, st));
+  HJ_CUDA(cudaEventSynchronize(P->ev1));
+  float ms = 0.f;
+  HJ_CUDA(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
+  const Ctrl c = *P->ctrl_h;
+  const long long cd = c.c_done;
+  if (x_dev) {
+    const void* X = P->X[cd & 1];
+    const int blocks = 4 * P->nsm;
+    if (g.dtype == HJ_F64)
+      extract_kernel<double><<<blocks, 256, 0, st>>>((const double*)X, g.pitch, g.dim, g.nx, g.ny, (int)g.col0, x_dev);
+    else
+      extract_kernel<float><<<blocks, 256, 0, st>>>((const float*)X, g.pitch, g.dim, g.nx, g.ny, (int)g.col0, x_dev);
+    HJ_CUDA(cudaGetLastError());
+  }
+  if (hist_dev) HJ_CUDA(cudaMemcpyAsync(hist_dev, P->hist, sizeof(double) * (cd + 1), cudaMemcpyDeviceToDevice, st));
+  HJ_CUDA(cudaStreamSynchronize(st));
+  res->cycles = cd;
+  res->converged = c.converged;
+  res->initial_residual = std::sqrt(c.S0) / g.h2;
+  res->final_residual = std::sqrt(c.S_last) / g.h2;
+  res->seconds_solve = ms * 1e-3;
+  // the plan is now "used": reset before another solve
+  return (hj_status)c.status;
+}
+
+void plan_free(hj_plan* P) {
+  if (!P) return;
+  for (auto& kv : P->graphs) cudaGraphExecDestroy(kv.second);
+  if (P->dist) dist_free(P);
+  cudaFree(P->X[0]);
+  cudaFree(P->X[1]);
+  cudaFree(P->H2F);
+  cudaFree(P->part);
+  cudaFree(P->rowpart);
+  cudaFree(P->rowpart_local);
+  cudaFree(P->hist);
+  cudaFree(P->ctrl);
+  cudaFree(P->bc_d);
+  cudaFree(P->x0_d);
+  if (P->ctrl_h) cudaFreeHost(P->ctrl_h);
+  for (auto ev : P->evpool) cudaEventDestroy(ev);
+  if (P->ev0) cudaEventDestroy(P->ev0);
+  if (P->ev1) cudaEventDestroy(P->ev1);
+  delete P;
+}
+
+}  // namespace hj
+
+// ==================================================================== C-ABI ==
+using namespace hj;
+
+extern "C" {
+
+const char* hj_last_error(void) { return g_last_error.c_str(); }
+
+hj_status hj_resource_figures(const hj_problem* pb, const hj_params* pr, int64_t* tiles,
+                              int64_t* threads, int64_t* smem) {
+  if (!tiles || !threads || !smem) { set_error("NULL output"); return HJ_ERR_INVALID_ARG; }
+  HJ_TRY(validate(pb, pr, false));
+  const long long esz = pr->dtype == HJ_F64 ? 8 : 4;
+  if (pr->mode == HJ_CLASSIC) {
+    *tiles = 0; *threads = pb->nx * pb->ny; *smem = 0;
+    return HJ_OK;
+  }
+  const long long tx = pr->tile_x, ty = pb->dim == 2 ? pr->tile_y : 1;
+  const long long ntx = (pb->nx + tx - 1) / tx, nty = pb->dim == 2 ? (pb->ny + ty - 1) / ty : 1;
+  *tiles = ntx * nty;
+  *threads = *tiles * tx * ty;
+  *smem = pb->dim == 1 ? esz * (2 * (tx + 2) + tx) : esz * (2 * (tx + 2) * (ty + 2) + tx * ty);
+  return HJ_OK;
+}
+
+hj_status hj_plan_create(const hj_problem* pb, const hj_params* pr, void* stream, hj_plan** plan) {
+  if (!plan) { set_error("NULL plan"); return HJ_ERR_INVALID_ARG; }
+  return plan_build(pb, pr, (cudaStream_t)stream, nullptr, plan);
+}
+hj_status hj_plan_create_dist(const hj_problem* pb, const hj_params* pr, const hj_dist* dist,
+                              void* stream, hj_plan** plan) {
+  if (!plan || !dist || !dist->nccl_id) { set_error("NULL argument"); return HJ_ERR_INVALID_ARG; }
+  HJ_TRY(validate_dist(pb, pr, dist));
+  DistInfo di{dist->rank, dist->nranks, dist->row_begin, dist->row_end, dist->nccl_id};
+  return plan_build(pb, pr, (cudaStream_t)stream, &di, plan);
+}
+hj_status hj_plan_reset(hj_plan* P) {
+  if (!P) { set_error("NULL plan"); return HJ_ERR_INVALID_ARG; }
+  return plan_reset(P);
+}
+hj_status hj_plan_run(hj_plan* P, int64_t ncycles, float* kernel_ms) {
+  if (!P) { set_error("NULL plan"); return HJ_ERR_INVALID_ARG; }
+  return plan_run(P, ncycles, kernel_ms);
+}
+hj_status hj_plan_solve(hj_plan* P, hj_result* res) {
+  if (!P || !res) { set_error("NULL argument"); return HJ_ERR_INVALID_ARG; }
+  return plan_solve(P, res, res->x, res->history);
+}
+int32_t hj_plan_launches_per_cycle(const hj_plan* P) { return P ? launches_per_cycle(P) : 0; }
+hj_status hj_plan_destroy(hj_plan* P) {
+  plan_free(P);
+  return HJ_OK;
+}
+
+hj_status jacobi_solve_device(const hj_problem* pb, const hj_params* pr, hj_result* res, void* stream) {
+  if (!res) { set_error("NULL result"); return HJ_ERR_INVALID_ARG; }
+  auto t0 = std::chrono::steady_clock::now();
+  hj_plan* P = nullptr;
+  HJ_TRY(plan_build(pb, pr, (cudaStream_t)stream, nullptr, &P));
+  hj_status s = plan_solve(P, res, res->x, res->history);
+  plan_free(P);
+  res->seconds_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return s;
+}
+
+hj_status jacobi_solve(const hj_problem* pb, const hj_params* pr, hj_result* res) {
+  if (!res || !res->x) { set_error("NULL result or result->x"); return HJ_ERR_INVALID_ARG; }
+  HJ_TRY(validate(pb, pr, true));
+  if (res->history && pr->max_cycles + 1 > HIST_CAP) {
+    set_error("history is limited to 2^24 cycles; pass history = NULL");
+    return HJ_ERR_INVALID_CONFIG;
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  const long long n = pb->nx * pb->ny;
+  const long long nbc = pb->dim == 1 ? 2 : 2 * pb->nx + 2 * pb->ny;
+  double *f = nullptr, *bc = nullptr, *x0 = nullptr, *x = nullptr, *hist = nullptr;
+  cudaStream_t st;
+  HJ_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  hj_status s = HJ_OK;
+  auto cleanup = [&]() {
+    cudaFree(f); cudaFree(bc); cudaFree(x0); cudaFree(x); cudaFree(hist);
+    cudaStreamDestroy(st);
+  };
+#define SCK(call)                                                                          \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      set_error(std::string(#call) + ": " + cudaGetErrorString(e_));                      \
+      cleanup();                                                                           \
+      return e_ == cudaErrorMemoryAllocation ? HJ_ERR_OOM : HJ_ERR_CUDA;                   \
+    }                                                                                      \
+  } while (0)
+  SCK(cudaMalloc(&f, sizeof(double) * n));
+  SCK(cudaMemcpyAsync(f, pb->f, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  if (pb->bc) {
+    SCK(cudaMalloc(&bc, sizeof(double) * nbc));
+    SCK(cudaMemcpyAsync(bc, pb->bc, sizeof(double) * nbc, cudaMemcpyHostToDevice, st));
+  }
+  if (pb->x0) {
+    SCK(cudaMalloc(&x0, sizeof(double) * n));
+    SCK(cudaMemcpyAsync(x0, pb->x0, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  }
+  SCK(cudaMalloc(&x, sizeof(double) * n));
+  if (res->history) SCK(cudaMalloc(&hist, sizeof(double) * (pr->max_cycles + 1)));
+  hj_problem dp = *pb;
+  dp.f = f;
+  dp.bc = bc;
+  dp.x0 = x0;
+  hj_plan* P = nullptr;
+  s = plan_build(&dp, pr, st, nullptr, &P);
+  if (s != HJ_OK) { cleanup(); return s; }
+  double* hx = res->x;
+  double* hh = res->history;
+  s = plan_solve(P, res, x, hist);
+  res->x = hx;
+  res->history = hh;
+  plan_free(P);
+  if (s == HJ_OK || s == HJ_NOT_CONVERGED || s == HJ_ERR_NUMERIC) {
+    SCK(cudaMemcpyAsync(hx, x, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    if (hh) SCK(cudaMemcpyAsync(hh, hist, sizeof(double) * (res->cycles + 1), cudaMemcpyDeviceToHost, st));
+    SCK(cudaStreamSynchronize(st));
+  }
+#undef SCK
+  cleanup();
+  res->seconds_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return s;
+}
+
+}  // extern "C"

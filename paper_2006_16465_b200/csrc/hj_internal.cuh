@@ -1,0 +1,176 @@
+// Internal declarations shared by the CUDA translation units of libhj.so.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/hj.h"
+
+namespace hj {
+
+// ------------------------------------------------------------------ errors ---
+void set_error(const std::string& msg);
+
+#define HJ_CUDA(call)                                                                     \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      ::hj::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));              \
+      return e_ == cudaErrorMemoryAllocation ? HJ_ERR_OOM : HJ_ERR_CUDA;                  \
+    }                                                                                     \
+  } while (0)
+
+#define HJ_TRY(expr)                  \
+  do {                                \
+    hj_status s_ = (expr);            \
+    if (s_ != HJ_OK) return s_;       \
+  } while (0)
+
+// --------------------------------------------------------- device control ----
+// One per plan, in device memory.  Written only by the finalize kernel (and reset by
+// the host); read by every cycle kernel so that cycles after convergence are no-ops.
+struct Ctrl {
+  long long c;          // index of the snapshot the next cycle kernel reads (x_c)
+  long long c_done;     // cycle at which the solve stopped
+  int done;             // 1 once converged / max_cycles reached / numeric error
+  int converged;
+  int status;           // hj_status of the solve
+  int pad;
+  double sqrtS0;        // sqrt(S_0) used by the relative test (or ref_residual * h^2)
+  double S0, S_last;    // h^2-scaled squared residuals
+};
+
+// Geometry of the padded iterate buffers (both dims; 1D uses one row).
+//   X[(j) * pitch + col0 - 1 + i],  i = 0..nx+1 along x (i=0: west/left ring),
+//   j = 0..ny+1 along y (j=0: south ring).  col0 = 2 puts interior column 0 on a
+//   16-byte boundary so that pairs of doubles are one 128-bit access.
+struct Geom {
+  int dim, dtype, mode, kernel_kind;
+  int64_t nx, ny;            // local interior extent (dist: the slab's rows)
+  int64_t pitch, col0, rows; // X layout (elements)
+  int64_t fpitch, frows;     // H2F layout: H2F[j*fpitch + i]
+  int tx, ty, k;
+  int64_t ntx, nty, ntiles;  // tiles of this plan (classic: row-blocks x col-blocks)
+  int64_t parts_per_row;     // partials per row group (= ntx)
+  int64_t nrg_local, rg_offset, nrg_global;  // row groups (tile rows) and their global offset
+  double h, h2;
+};
+
+enum KernelKind { K_REG2D = 0, K_SMEM2D = 1, K_CLASSIC2D = 2, K_REG1D = 3, K_SMEM1D = 4, K_CLASSIC1D = 5 };
+
+// Kernel launch descriptor passed to the per-dimension launchers.
+struct CycleArgs {
+  const void* xin;
+  void* xout;
+  const void* h2f;
+  const CUtensorMap* tm_in;   // TMA descriptor of xin (REG2D)
+  const CUtensorMap* tm_f;    // TMA descriptor of h2f (REG2D)
+  double* part;               // per-tile residual partials of the snapshot
+  const Ctrl* ctrl;
+  long long max_cycles;
+};
+
+// Launchers (kernels_2d.cu / kernels_1d.cu).  Return cudaGetLastError().
+cudaError_t launch_cycle_2d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st);
+cudaError_t launch_cycle_1d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st);
+size_t reg2d_smem_bytes(int dtype);
+int reg2d_warps_per_cta(int dtype);
+size_t reg1d_smem_bytes(int dtype, int tile);
+int reg1d_warps_per_cta(int dtype, int tile);
+cudaError_t reg_kernels_configure();  // opt in to large dynamic shared memory
+
+// Classic kernels block geometry (partials per 16-row x 256-col block).
+constexpr int CLASSIC2D_ROWS = 16;
+constexpr int CLASSIC2D_COLS = 256;   // 128 threads x 2 columns
+constexpr int CLASSIC1D_CELLS = 2048; // 256 threads x 8 cells
+
+// ------------------------------------------------------------- PTX helpers ---
+#if defined(__CUDACC__)
+__host__ __device__ __forceinline__ long long lmin(long long a, long long b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 2D tensor tile global -> shared, completion on an mbarrier (TMA, SASS UTMALDG).
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// Contiguous bulk copy global -> shared (TMA bulk engine, SASS UBLKCP); 16-B aligned, size % 16 == 0.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* tm) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
+}
+
+// Canonical elemental updates, see DESIGN.md §6:
+//   1D: 0.5 * ((L + R) + h2f)  ==  fma(0.5, L + R, q),   q = 0.5 * h2f  (exact)
+//   2D: 0.25 * (((W + E) + (S + N)) + h2f) == fma(0.25, (W+E)+(S+N), q), q = 0.25 * h2f
+// Scaling by a power of two commutes with round-to-nearest (no under/overflow), so the
+// single-rounding fma equals the two-rounding form bit for bit.
+__device__ __forceinline__ double upd2(double w, double e, double s, double n, double q) {
+  return __fma_rn(0.25, __dadd_rn(__dadd_rn(w, e), __dadd_rn(s, n)), q);
+}
+__device__ __forceinline__ float upd2(float w, float e, float s, float n, float q) {
+  return __fmaf_rn(0.25f, __fadd_rn(__fadd_rn(w, e), __fadd_rn(s, n)), q);
+}
+__device__ __forceinline__ double upd1(double l, double r, double q) {
+  return __fma_rn(0.5, __dadd_rn(l, r), q);
+}
+__device__ __forceinline__ float upd1(float l, float r, float q) {
+  return __fmaf_rn(0.5f, __fadd_rn(l, r), q);
+}
+// h^2-scaled residual contributions in double (h2f64 = h2f of the iterate type, widened).
+__device__ __forceinline__ double res2(double x, double w, double e, double s, double n, double h2f) {
+  return h2f - (4.0 * x - ((w + e) + (s + n)));
+}
+__device__ __forceinline__ double res1(double x, double l, double r, double h2f) {
+  return h2f - (2.0 * x - (l + r));
+}
+template <typename T>
+__device__ __forceinline__ T qscale2(T h2f) { return T(0.25) * h2f; }
+template <typename T>
+__device__ __forceinline__ T qscale1(T h2f) { return T(0.5) * h2f; }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+#endif
+
+}  // namespace hj

@@ -1,0 +1,73 @@
+// The plan object behind hj_plan* (engine.cu) and the distributed hooks (dist.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <vector>
+
+#include "hj_internal.cuh"
+
+struct DistState;  // dist.cu
+
+namespace hj {
+
+struct DistInfo {
+  int rank, nranks;
+  long long row_begin, row_end;
+  const char* nccl_id;  // 128 bytes
+};
+
+}  // namespace hj
+
+struct hj_plan {
+  hj::Geom g{};
+  hj_params prm{};
+  int nsm = 0;
+  cudaStream_t stream = nullptr;
+  long long ny_global = 0, gy0 = 0;
+  void* X[2] = {nullptr, nullptr};
+  void* H2F = nullptr;
+  double* part = nullptr;
+  double* rowpart = nullptr;        // per row group sums, global length (input of finalize)
+  double* rowpart_local = nullptr;  // dist: this rank's row groups, zeros elsewhere
+  double* rowsum_dst = nullptr;     // where rowsum writes (rowpart, or rowpart_local in dist)
+  double* hist = nullptr;
+  long long hist_cap = 0;
+  hj::Ctrl* ctrl = nullptr;
+  hj::Ctrl* ctrl_h = nullptr;
+  double* bc_d = nullptr;
+  double* x0_d = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  CUtensorMap tmX[2];
+  CUtensorMap tmF;
+  std::map<int, cudaGraphExec_t> graphs;
+  long long c_host = 0;
+  std::vector<cudaEvent_t> evpool;  // timed runs: (start, end) per cycle kernel
+  int evused = 0;
+  DistState* dist = nullptr;
+};
+
+namespace hj {
+
+constexpr long long HIST_CAP = 1LL << 24;
+
+hj_status validate(const hj_problem* pb, const hj_params* pr, bool need_f);
+hj_status validate_dist(const hj_problem* pb, const hj_params* pr, const hj_dist* dist);
+hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st, const DistInfo* di,
+                     hj_plan** out);
+hj_status plan_reset(hj_plan* P);
+hj_status plan_run(hj_plan* P, long long ncycles, float* kernel_ms);
+hj_status plan_solve(hj_plan* P, hj_result* res, double* x_dev, double* hist_dev);
+void plan_free(hj_plan* P);
+int launches_per_cycle(const hj_plan* P);
+
+// dist.cu
+hj_status dist_create(hj_plan* P, const DistInfo* di);
+hj_status dist_initial_exchange(hj_plan* P);
+hj_status dist_halo_exchange(hj_plan* P, int buf);
+hj_status dist_allreduce(hj_plan* P);
+void dist_free(hj_plan* P);
+
+}  // namespace hj

@@ -1,0 +1,320 @@
+// 1D kernels of libhj.so: one hierarchical cycle (two designs) and one classic sweep.
+//
+// PAPER.md:161-166 (§3.3) and Appendix A (:532-575): each block copies its subdomain plus one
+// point left and right to on-chip memory, performs k sub-iterations of the update
+// x_i <- (b_i dx^2 + x_{i-1} + x_{i+1})/2 with the two halo points frozen, and
+// writes the interior back.  Residual of the snapshot fused: s = h2f - (2x - (L+R)).
+#include "hj_internal.cuh"
+
+namespace hj {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// =============================================================================
+// REG1D — warp per tile of T = 32*C points; lane l holds points C*l..C*l+C-1 in registers,
+// neighbours across lanes by one shuffle each way per sub-iteration; tile + halo staged in
+// shared memory by the TMA bulk-copy engine (cp.async.bulk), double-buffered per warp.
+// =============================================================================
+template <typename T, int C>
+struct R1 {
+  static constexpr int TILE = 32 * C;
+  static constexpr int COL0 = 16 / sizeof(T);
+  static constexpr int XN = TILE + 2 * COL0;                  // elements copied for x (16-B multiple)
+  static constexpr int XBYTES = XN * sizeof(T);
+  static constexpr int XSLOT = (XBYTES + 127) / 128 * 128;
+  static constexpr int FBYTES = TILE * sizeof(T);
+  static constexpr int SLOT = XSLOT + (FBYTES + 127) / 128 * 128;
+  static constexpr int WARPS = 4;
+  static constexpr size_t SMEM = 128 + 128 + size_t(WARPS) * 2 * SLOT;
+};
+
+template <typename T, int C, bool RAGGED>
+__device__ __forceinline__ void reg1d_tile(const T* __restrict__ sx, const T* __restrict__ sf,
+                                           T* __restrict__ xout, long long t, int w, int lane,
+                                           int kk, double* __restrict__ part, uint64_t* bar,
+                                           const T* __restrict__ xin, const T* __restrict__ h2f,
+                                           long long t_next, void* slot_x, void* slot_f) {
+  using P = R1<T, C>;
+  T x[C], q[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    x[c] = sx[P::COL0 + C * lane + c];
+    q[c] = qscale1<T>(sf[C * lane + c]);
+  }
+  const T hl = sx[P::COL0 - 1];       // frozen left halo (used by lane 0)
+  const T hr = sx[P::COL0 + P::TILE]; // frozen right halo (used by lane 31) — for a ragged
+                                      // tile the right halo is x[w] (the ring), kept frozen below
+  uint32_t act = 0xffffffffu;
+  if (RAGGED) {
+    act = 0;
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (C * lane + c < w) act |= 1u << c;
+  }
+  // fused residual of the snapshot
+  double acc = 0.0;
+  {
+    T l = __shfl_up_sync(FULL, x[C - 1], 1);
+    T r = __shfl_down_sync(FULL, x[0], 1);
+    if (lane == 0) l = hl;
+    if (lane == 31) r = hr;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const T L = c == 0 ? l : x[c - 1];
+      const T R = c == C - 1 ? r : x[c + 1];
+      const double s = res1((double)x[c], (double)L, (double)R, (double)(T(2) * q[c]));
+      if ((act >> c) & 1u) acc = __fma_rn(s, s, acc);
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) part[t] = acc;
+  __syncwarp();
+  if (lane == 0 && t_next >= 0) {
+    mbar_arrive_expect_tx(bar, P::XBYTES + P::FBYTES);
+    bulk_load(slot_x, xin + t_next * P::TILE, P::XBYTES, bar);
+    bulk_load(slot_f, h2f + t_next * P::TILE, P::FBYTES, bar);
+  }
+#pragma unroll 1
+  for (int s = 0; s < kk; ++s) {
+    T l = __shfl_up_sync(FULL, x[C - 1], 1);
+    T r = __shfl_down_sync(FULL, x[0], 1);
+    if (lane == 0) l = hl;
+    if (lane == 31) r = hr;
+    T prev = l;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const T R = c == C - 1 ? r : x[c + 1];
+      const T nv = upd1(prev, R, q[c]);
+      prev = x[c];
+      if (!RAGGED || ((act >> c) & 1u)) x[c] = nv;
+    }
+  }
+  if (kk == 0) return;
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    if (!RAGGED || ((act >> c) & 1u)) xout[P::COL0 + t * P::TILE + C * lane + c] = x[c];
+}
+
+template <typename T, int C>
+__global__ void __launch_bounds__(R1<T, C>::WARPS * 32)
+reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restrict__ h2f, int nx,
+             long long ntiles, double* __restrict__ part, const Ctrl* __restrict__ ctrl, int k,
+             long long max_cycles) {
+  using P = R1<T, C>;
+  if (ctrl->done) return;
+  const int kk = (ctrl->c >= max_cycles) ? 0 : k;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base) + 2 * warp;
+  unsigned char* slot0 = base + 128 + size_t(warp) * 2 * P::SLOT;
+  unsigned char* slot1 = slot0 + P::SLOT;
+  const long long gw = (long long)blockIdx.x * P::WARPS + warp;
+  const long long nw = (long long)gridDim.x * P::WARPS;
+  if (gw >= ntiles) return;
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    for (int s = 0; s < 2; ++s) {
+      const long long t = gw + s * nw;
+      if (t < ntiles) {
+        unsigned char* sl = s ? slot1 : slot0;
+        mbar_arrive_expect_tx(&bars[s], P::XBYTES + P::FBYTES);
+        bulk_load(sl, xin + t * P::TILE, P::XBYTES, &bars[s]);
+        bulk_load(sl + P::XSLOT, h2f + t * P::TILE, P::FBYTES, &bars[s]);
+      }
+    }
+  }
+  __syncwarp();
+  int it = 0;
+  for (long long t = gw; t < ntiles; t += nw, ++it) {
+    const int s = it & 1;
+    unsigned char* sl = s ? slot1 : slot0;
+    mbar_wait(&bars[s], (it >> 1) & 1);
+    const int w = (int)lmin(P::TILE, nx - t * P::TILE);
+    const long long tn = t + 2 * nw < ntiles ? t + 2 * nw : -1;
+    const T* sx = reinterpret_cast<const T*>(sl);
+    const T* sf = reinterpret_cast<const T*>(sl + P::XSLOT);
+    if (w == P::TILE)
+      reg1d_tile<T, C, false>(sx, sf, xout, t, w, lane, kk, part, &bars[s], xin, h2f, tn, sl, sl + P::XSLOT);
+    else
+      reg1d_tile<T, C, true>(sx, sf, xout, t, w, lane, kk, part, &bars[s], xin, h2f, tn, sl, sl + P::XSLOT);
+  }
+}
+
+// =============================================================================
+// SMEM1D — the paper's Appendix A design: blockDim.x = T threads, shared memory
+// [container 0 (T+2) | container 1 (T+2) | rhs (T)], __syncthreads per
+// sub-iteration, write-back of the latest container (reading c8), into the other global
+// buffer (reading c6), rhs of the updated point (reading c7).
+// =============================================================================
+template <typename T>
+__global__ void smem1d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
+                              const T* __restrict__ h2f, int nx, double* __restrict__ part,
+                              const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
+  if (ctrl->done) return;
+  const int kk = (ctrl->c >= max_cycles) ? 0 : k;
+  constexpr int COL0 = 16 / sizeof(T);
+  const int Tn = blockDim.x, L = Tn + 2;
+  extern __shared__ unsigned char smem_raw[];
+  T* A = reinterpret_cast<T*>(smem_raw);
+  T* B = A + L;
+  T* rhs = B + L;
+  __shared__ double wsum[32];
+  const long long t = blockIdx.x;
+  const long long i0 = t * Tn;
+  const int w = (int)lmin(Tn, nx - i0);
+  const int a = threadIdx.x;
+  for (int q = a; q < L; q += Tn) {
+    const long long gi = i0 + q;  // padded index, 0 = left ring
+    const T v = gi <= nx + 1 ? xin[COL0 - 1 + gi] : T(0);
+    A[q] = v;
+    B[q] = v;
+  }
+  const bool active = a < w;
+  if (active) rhs[a] = h2f[i0 + a];
+  __syncthreads();
+  double s2 = 0.0;
+  if (active) {
+    const double s = res1((double)A[a + 1], (double)A[a], (double)A[a + 2], (double)rhs[a]);
+    s2 = s * s;
+  }
+  s2 = warp_sum(s2);
+  if ((a & 31) == 0) wsum[a >> 5] = s2;
+  __syncthreads();
+  if (a == 0) {
+    double acc = 0.0;
+    for (int q = 0; q < (Tn + 31) / 32; ++q) acc += wsum[q];
+    part[t] = acc;
+  }
+  const T q2 = active ? qscale1<T>(rhs[a]) : T(0);
+  T* cur = A;
+  T* nxt = B;
+  for (int s = 0; s < kk; ++s) {
+    if (active) nxt[a + 1] = upd1(cur[a], cur[a + 2], q2);
+    __syncthreads();
+    T* tmp = cur; cur = nxt; nxt = tmp;
+  }
+  if (kk > 0 && active) xout[COL0 + i0 + a] = cur[a + 1];
+}
+
+// =============================================================================
+// CLASSIC1D — one sweep; 256 threads x 8 consecutive points per CTA (128-bit loads),
+// neighbours by shuffle, fused residual, one partial per CTA.
+// =============================================================================
+template <typename T>
+__global__ void __launch_bounds__(256)
+classic1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restrict__ h2f, int nx,
+                 double* __restrict__ part, const Ctrl* __restrict__ ctrl, long long max_cycles) {
+  if (ctrl->done) return;
+  const bool write = ctrl->c < max_cycles;
+  constexpr int COL0 = 16 / sizeof(T);
+  constexpr int V = 8;
+  __shared__ double wsum[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long i0 = (long long)blockIdx.x * CLASSIC1D_CELLS + (long long)threadIdx.x * V;
+  T x[V], f[V];
+#pragma unroll
+  for (int c = 0; c < V; ++c) {
+    const long long i = i0 + c;
+    x[c] = i <= nx ? xin[COL0 + i] : T(0);   // interior or right ring
+    f[c] = i < nx ? h2f[i] : T(0);
+  }
+  T l = __shfl_up_sync(FULL, x[V - 1], 1);
+  T r = __shfl_down_sync(FULL, x[0], 1);
+  if (lane == 0 && i0 <= nx + 1) l = xin[COL0 + i0 - 1];
+  if (lane == 31 && i0 + V <= nx) r = xin[COL0 + i0 + V];
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c < V; ++c) {
+    const long long i = i0 + c;
+    const T L = c == 0 ? l : x[c - 1];
+    const T R = c == V - 1 ? r : x[c + 1];
+    if (i < nx) {
+      const double s = res1((double)x[c], (double)L, (double)R, (double)f[c]);
+      acc = __fma_rn(s, s, acc);
+      if (write) xout[COL0 + i] = upd1(L, R, qscale1<T>(f[c]));
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) wsum[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < 8; ++q) s += wsum[q];
+    part[blockIdx.x] = s;
+  }
+}
+
+template <typename T, int C>
+void launch_reg1d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
+  using P = R1<T, C>;
+  long long ctas = (g.ntiles + P::WARPS - 1) / P::WARPS;
+  if (ctas > grid_hint) ctas = grid_hint;
+  reg1d_kernel<T, C><<<(unsigned)ctas, P::WARPS * 32, P::SMEM, st>>>(
+      (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (int)g.nx, g.ntiles, a.part, a.ctrl, g.k,
+      a.max_cycles);
+}
+
+template <typename T>
+cudaError_t launch_1d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
+  if (g.kernel_kind == K_REG1D) {
+    switch (g.tx / 32) {
+      case 1: launch_reg1d<T, 1>(g, a, grid_hint * 8, st); break;
+      case 2: launch_reg1d<T, 2>(g, a, grid_hint * 8, st); break;
+      case 4: launch_reg1d<T, 4>(g, a, grid_hint * 4, st); break;
+      case 8: launch_reg1d<T, 8>(g, a, grid_hint * 4, st); break;
+      case 16: launch_reg1d<T, 16>(g, a, grid_hint * 2, st); break;
+      case 32: launch_reg1d<T, 32>(g, a, grid_hint, st); break;
+      default: return cudaErrorInvalidValue;
+    }
+  } else if (g.kernel_kind == K_SMEM1D) {
+    const size_t smem = sizeof(T) * (2 * size_t(g.tx + 2) + size_t(g.tx));
+    smem1d_kernel<T><<<(unsigned)g.ntiles, g.tx, smem, st>>>((const T*)a.xin, (T*)a.xout,
+                                                              (const T*)a.h2f, (int)g.nx, a.part,
+                                                              a.ctrl, g.k, a.max_cycles);
+  } else {
+    classic1d_kernel<T><<<(unsigned)g.ntiles, 256, 0, st>>>((const T*)a.xin, (T*)a.xout,
+                                                             (const T*)a.h2f, (int)g.nx, a.part,
+                                                             a.ctrl, a.max_cycles);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T, int C>
+cudaError_t cfg1() {
+  return cudaFuncSetAttribute(reg1d_kernel<T, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)R1<T, C>::SMEM);
+}
+
+}  // namespace
+
+size_t reg1d_smem_bytes(int dtype, int tile) {
+  (void)tile;
+  return dtype == HJ_F64 ? R1<double, 32>::SMEM : R1<float, 32>::SMEM;
+}
+int reg1d_warps_per_cta(int, int) { return 4; }
+
+cudaError_t configure_1d() {
+  cudaError_t e = cudaSuccess;
+#define HJ_CFG(T)                                                                              \
+  if ((e = cfg1<T, 1>()) != cudaSuccess || (e = cfg1<T, 2>()) != cudaSuccess ||                \
+      (e = cfg1<T, 4>()) != cudaSuccess || (e = cfg1<T, 8>()) != cudaSuccess ||                \
+      (e = cfg1<T, 16>()) != cudaSuccess || (e = cfg1<T, 32>()) != cudaSuccess)                \
+    return e;
+  HJ_CFG(double)
+  HJ_CFG(float)
+#undef HJ_CFG
+  return cudaSuccess;
+}
+
+cudaError_t launch_cycle_1d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
+  return g.dtype == HJ_F64 ? launch_1d_t<double>(g, a, grid_hint, st)
+                           : launch_1d_t<float>(g, a, grid_hint, st);
+}
+
+}  // namespace hj

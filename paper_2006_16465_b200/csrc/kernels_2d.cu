@@ -1,0 +1,449 @@
+// 2D kernels of libhj.so: one hierarchical cycle (two kernel designs) and one classic sweep.
+//
+// PAPER.md:380-387 (§4.1): a cycle copies every (Tx+2)x(Ty+2) augmented subdomain from global
+// to on-chip memory, runs k Jacobi sub-iterations on the Tx x Ty interior with the halo frozen,
+// and copies the interior back.  PAPER.md:114-133 (§3.2): the classic sweep.
+// Every kernel also reduces the h^2-scaled residual of the snapshot it reads:
+// s = h2f - (4x - ((W+E)+(S+N))), sum of s^2 per tile -> part[tile].
+#include "hj_internal.cuh"
+
+namespace hj {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <typename T> struct VecOf;
+template <> struct VecOf<double> { using v2 = double2; };
+template <> struct VecOf<float> { using v2 = float2; };
+
+// =============================================================================
+// REG2D — the B200 design for 32x32 tiles.  One warp owns one tile; the tile lives in
+// registers: lane l holds rows 8*(l>>3)..+7 and columns 4*(l&7)..+3 of the interior
+// (32 cells), so a sub-iteration is 4 FP64 ops per cell plus warp shuffles for the
+// 4x8-lane block edges; the frozen halo sits in registers of the edge lanes.
+// Each warp double-buffers its next tiles in shared memory with TMA
+// (cp.async.bulk.tensor.2d, completion on a per-slot mbarrier), so HBM traffic for the
+// next tile overlaps the k sub-iterations of the current one.  Persistent grid.
+// =============================================================================
+template <typename T>
+struct R2 {
+  static constexpr int COL0 = 16 / sizeof(T);                          // interior column offset
+  static constexpr int BW = ((COL0 + 33) + (16 / sizeof(T)) - 1) / (16 / sizeof(T)) * (16 / sizeof(T));
+  static constexpr int BH = 34;
+  static constexpr int XBYTES = BW * BH * sizeof(T);
+  static constexpr int XSLOT = (XBYTES + 127) / 128 * 128;
+  static constexpr int FBYTES = 32 * 32 * sizeof(T);
+  static constexpr int SLOT = XSLOT + FBYTES;
+  static constexpr int WARPS = sizeof(T) == 8 ? 6 : 12;
+  static constexpr int BARS = 128;                                      // barrier region bytes
+  static constexpr size_t SMEM = 128 + BARS + size_t(WARPS) * 2 * SLOT; // +128 for alignment
+};
+
+template <typename T, bool RAGGED>
+struct Tile2 {
+  T x[8][4];   // current iterate
+  T q[8][4];   // 0.25 * h^2 f
+  T hx[8];     // frozen W halo (lx == 0) or E halo (lx == 7) of my 8 rows
+  T hy[4];     // frozen S halo (ly == 0) or N halo (ly == 3) of my 4 columns
+  uint32_t act; // RAGGED: bit 4*i+c set if cell (i, c) is inside the tile
+
+  __device__ __forceinline__ bool on(int i, int c) const {
+    return !RAGGED || ((act >> (4 * i + c)) & 1u);
+  }
+
+  // Residual of the snapshot, s^2 summed over my cells (double).
+  __device__ __forceinline__ double residual(int lx, int ly) const {
+    T up[4], dn[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      up[c] = __shfl_down_sync(FULL, x[0][c], 8);
+      dn[c] = __shfl_up_sync(FULL, x[7][c], 8);
+      if (ly == 3) up[c] = hy[c];
+      if (ly == 0) dn[c] = hy[c];
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      T w = __shfl_up_sync(FULL, x[i][3], 1, 8);
+      T e = __shfl_down_sync(FULL, x[i][0], 1, 8);
+      if (lx == 0) w = hx[i];
+      if (lx == 7) e = hx[i];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const T W = c == 0 ? w : x[i][c - 1];
+        const T E = c == 3 ? e : x[i][c + 1];
+        const T S = i == 0 ? dn[c] : x[i - 1][c];
+        const T N = i == 7 ? up[c] : x[i + 1][c];
+        const double s = res2((double)x[i][c], (double)W, (double)E, (double)S, (double)N,
+                              (double)(T(4) * q[i][c]));
+        if (on(i, c)) acc = __fma_rn(s, s, acc);
+      }
+    }
+    return acc;
+  }
+
+  // One Jacobi sub-iteration, rows processed top-down (DOWN) or bottom-up, keeping only
+  // one saved old row; alternating directions lets the register allocator rotate names.
+  template <bool DOWN>
+  __device__ __forceinline__ void sweep(int lx, int ly) {
+    T up[4], dn[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      up[c] = __shfl_down_sync(FULL, x[0][c], 8);   // row 0 of the lane below -> my N of row 7
+      dn[c] = __shfl_up_sync(FULL, x[7][c], 8);     // row 7 of the lane above -> my S of row 0
+      if (ly == 3) up[c] = hy[c];
+      if (ly == 0) dn[c] = hy[c];
+    }
+    T saved[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) saved[c] = DOWN ? dn[c] : up[c];
+#pragma unroll
+    for (int ii = 0; ii < 8; ++ii) {
+      const int i = DOWN ? ii : 7 - ii;
+      T w = __shfl_up_sync(FULL, x[i][3], 1, 8);
+      T e = __shfl_down_sync(FULL, x[i][0], 1, 8);
+      if (lx == 0) w = hx[i];
+      if (lx == 7) e = hx[i];
+      T nw[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const T W = c == 0 ? w : x[i][c - 1];
+        const T E = c == 3 ? e : x[i][c + 1];
+        const T S = DOWN ? saved[c] : (i == 0 ? dn[c] : x[i - 1][c]);
+        const T N = DOWN ? (i == 7 ? up[c] : x[i + 1][c]) : saved[c];
+        nw[c] = upd2(W, E, S, N, q[i][c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        saved[c] = x[i][c];
+        x[i][c] = on(i, c) ? nw[c] : x[i][c];
+      }
+    }
+  }
+};
+
+template <typename T, bool RAGGED>
+__device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __restrict__ sf,
+                                           T* __restrict__ xout, long long pitch, long long tx,
+                                           long long ty, int w, int hgt, int lane, int kk,
+                                           double* __restrict__ part, long long t,
+                                           uint64_t* bar_reissue, const CUtensorMap* tmX,
+                                           const CUtensorMap* tmF, long long t_next, int ntx,
+                                           void* slot_x, void* slot_f) {
+  using C = R2<T>;
+  const int lx = lane & 7, ly = lane >> 3;
+  Tile2<T, RAGGED> tl;
+  // shared -> registers
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = 8 * ly + i;
+    const T* rowx = sx + (r + 1) * C::BW + C::COL0 + 4 * lx;
+    const T* rowf = sf + r * 32 + 4 * lx;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      tl.x[i][c] = rowx[c];
+      tl.q[i][c] = qscale2<T>(rowf[c]);
+    }
+    tl.hx[i] = sx[(r + 1) * C::BW + (lx == 0 ? C::COL0 - 1 : C::COL0 + 32)];
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) tl.hy[c] = sx[(ly == 0 ? 0 : 33) * C::BW + C::COL0 + 4 * lx + c];
+  tl.act = 0;
+  if (RAGGED) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (8 * ly + i < hgt && 4 * lx + c < w) tl.act |= 1u << (4 * i + c);
+  }
+  // fused residual of the snapshot (consumes every loaded value)
+  double acc = warp_sum(tl.residual(lx, ly));
+  if (lane == 0) part[t] = acc;
+  __syncwarp();
+  // the slot is free: prefetch the tile after next into it
+  if (lane == 0 && t_next >= 0) {
+    const long long nx_ = t_next % ntx, ny_ = t_next / ntx;
+    mbar_arrive_expect_tx(bar_reissue, C::XBYTES + C::FBYTES);
+    tma_load_2d(slot_x, tmX, (int)(32 * nx_), (int)(32 * ny_), bar_reissue);
+    tma_load_2d(slot_f, tmF, (int)(32 * nx_), (int)(32 * ny_), bar_reissue);
+  }
+  // k sub-iterations, halo frozen
+  int s = 0;
+#pragma unroll 1
+  for (; s + 1 < kk; s += 2) {
+    tl.template sweep<true>(lx, ly);
+    tl.template sweep<false>(lx, ly);
+  }
+  if (s < kk) tl.template sweep<true>(lx, ly);
+  if (kk == 0) return;  // residual-only pass (after max_cycles)
+  // registers -> global (interior of the NEXT iterate; snapshot semantics)
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const long long r = 32 * ty + 8 * ly + i;
+    T* dst = xout + (r + 1) * pitch + C::COL0 + 32 * tx + 4 * lx;
+    if (!RAGGED) {
+      using V2 = typename VecOf<T>::v2;
+      reinterpret_cast<V2*>(dst)[0] = V2{tl.x[i][0], tl.x[i][1]};
+      reinterpret_cast<V2*>(dst)[1] = V2{tl.x[i][2], tl.x[i][3]};
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (tl.on(i, c)) dst[c] = tl.x[i][c];
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(R2<T>::WARPS * 32, 1)
+reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
+             T* __restrict__ xout, long long pitch, int nx, int ny, int ntx, long long ntiles,
+             double* __restrict__ part, const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
+  using C = R2<T>;
+  if (ctrl->done) return;
+  const int kk = (ctrl->c >= max_cycles) ? 0 : k;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base) + 2 * warp;
+  unsigned char* slot0 = base + C::BARS + size_t(warp) * 2 * C::SLOT;
+  unsigned char* slot1 = slot0 + C::SLOT;
+  const long long gw = (long long)blockIdx.x * C::WARPS + warp;
+  const long long nw = (long long)gridDim.x * C::WARPS;
+  if (gw >= ntiles) return;
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    prefetch_tensormap(&tmX);
+    prefetch_tensormap(&tmF);
+    for (int s = 0; s < 2; ++s) {
+      const long long t = gw + s * nw;
+      if (t < ntiles) {
+        unsigned char* sl = s ? slot1 : slot0;
+        mbar_arrive_expect_tx(&bars[s], C::XBYTES + C::FBYTES);
+        tma_load_2d(sl, &tmX, (int)(32 * (t % ntx)), (int)(32 * (t / ntx)), &bars[s]);
+        tma_load_2d(sl + C::XSLOT, &tmF, (int)(32 * (t % ntx)), (int)(32 * (t / ntx)), &bars[s]);
+      }
+    }
+  }
+  __syncwarp();
+  int it = 0;
+  for (long long t = gw; t < ntiles; t += nw, ++it) {
+    const int s = it & 1;
+    unsigned char* sl = s ? slot1 : slot0;
+    mbar_wait(&bars[s], (it >> 1) & 1);
+    const long long tx = t % ntx, ty = t / ntx;
+    const int w = (int)lmin(32, nx - 32 * tx), hgt = (int)lmin(32, ny - 32 * ty);
+    const long long tn = t + 2 * nw < ntiles ? t + 2 * nw : -1;
+    const T* sx = reinterpret_cast<const T*>(sl);
+    const T* sf = reinterpret_cast<const T*>(sl + C::XSLOT);
+    if (w == 32 && hgt == 32)
+      reg2d_tile<T, false>(sx, sf, xout, pitch, tx, ty, w, hgt, lane, kk, part, t, &bars[s], &tmX,
+                           &tmF, tn, ntx, sl, sl + C::XSLOT);
+    else
+      reg2d_tile<T, true>(sx, sf, xout, pitch, tx, ty, w, hgt, lane, kk, part, t, &bars[s], &tmX,
+                          &tmF, tn, ntx, sl, sl + C::XSLOT);
+  }
+}
+
+// =============================================================================
+// SMEM2D — the paper's design (App. A): one CTA per tile, one thread per
+// DOF, two (Tx+2)(Ty+2) containers plus a Tx*Ty rhs array in shared memory (exactly the
+// paper's byte formula), __syncthreads between sub-iterations.  Any tile shape with
+// Tx*Ty <= 1024.  Used for tile shapes REG2D does not cover and as the in-tile baseline.
+// =============================================================================
+template <typename T>
+__global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
+                              const T* __restrict__ h2f, long long pitch, long long fpitch, int nx,
+                              int ny, int ntx, double* __restrict__ part,
+                              const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
+  if (ctrl->done) return;
+  const int kk = (ctrl->c >= max_cycles) ? 0 : k;
+  constexpr int COL0 = 16 / sizeof(T);
+  const int Tx = blockDim.x, Ty = blockDim.y, L = Tx + 2;
+  extern __shared__ unsigned char smem_raw[];
+  T* A = reinterpret_cast<T*>(smem_raw);
+  T* B = A + L * (Ty + 2);
+  T* rhs = B + L * (Ty + 2);
+  __shared__ double wsum[32];
+  const long long t = blockIdx.x;
+  const long long tx = t % ntx, ty = t / ntx;
+  const long long i0 = tx * Tx, j0 = ty * Ty;  // interior origin (0-based)
+  const int w = (int)lmin(Tx, nx - i0), hgt = (int)lmin(Ty, ny - j0);
+  const int tid = threadIdx.y * Tx + threadIdx.x, nth = Tx * Ty;
+  // Step 1: augmented subdomain into both containers (App. A :549-556)
+  for (int q = tid; q < L * (Ty + 2); q += nth) {
+    const int a = q % L, b = q / L;          // a: 0..Tx+1, b: 0..Ty+1 (halo included)
+    const long long gi = i0 + a, gj = j0 + b; // padded coordinates (ring at 0)
+    T v = T(0);
+    if (gi <= nx + 1 && gj <= ny + 1) v = xin[gj * pitch + (COL0 - 1) + gi];
+    A[q] = v;
+    B[q] = v;
+  }
+  const int a = threadIdx.x, b = threadIdx.y;
+  const bool active = a < w && b < hgt;
+  if (active) rhs[b * Tx + a] = h2f[(j0 + b) * fpitch + i0 + a];
+  __syncthreads();
+  // fused residual of the snapshot
+  double s2 = 0.0;
+  const int c = (b + 1) * L + (a + 1);
+  if (active) {
+    const double s = res2((double)A[c], (double)A[c - 1], (double)A[c + 1], (double)A[c - L],
+                          (double)A[c + L], (double)rhs[b * Tx + a]);
+    s2 = s * s;
+  }
+  s2 = warp_sum(s2);
+  if ((tid & 31) == 0) wsum[tid >> 5] = s2;
+  __syncthreads();
+  if (tid == 0) {
+    double acc = 0.0;
+    for (int q = 0; q < (nth + 31) / 32; ++q) acc += wsum[q];
+    part[t] = acc;
+  }
+  // Step 2: k sub-iterations, ping-pong between the containers, halo frozen
+  const T q4 = active ? qscale2<T>(rhs[b * Tx + a]) : T(0);
+  T* cur = A;
+  T* nxt = B;
+  for (int s = 0; s < kk; ++s) {
+    if (active) nxt[c] = upd2(cur[c - 1], cur[c + 1], cur[c - L], cur[c + L], q4);
+    __syncthreads();
+    T* tmp = cur; cur = nxt; nxt = tmp;
+  }
+  // Step 3: interior back to global (the next iterate)
+  if (kk > 0 && active) xout[(j0 + b + 1) * pitch + COL0 + i0 + a] = cur[c];
+}
+
+// =============================================================================
+// CLASSIC2D — one Jacobi sweep over the grid, HBM-bound (24 B/cell f64):
+// a CTA of 128 threads covers 256 columns x 16 rows, each lane two adjacent columns with
+// 128-bit (f64) loads; W/E neighbours by warp shuffle, N/S from the 18 rows held in registers.
+// Fused residual of the snapshot, one partial per CTA.
+// =============================================================================
+template <typename T>
+__global__ void __launch_bounds__(128)
+classic2d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restrict__ h2f,
+                 long long pitch, long long fpitch, int nx, int ny, int ncb,
+                 double* __restrict__ part, const Ctrl* __restrict__ ctrl, long long max_cycles) {
+  if (ctrl->done) return;
+  const bool write = ctrl->c < max_cycles;
+  constexpr int COL0 = 16 / sizeof(T);
+  constexpr int R = CLASSIC2D_ROWS;
+  __shared__ double wsum[4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long cb = blockIdx.x % ncb, rb = blockIdx.x / ncb;
+  const long long i = cb * CLASSIC2D_COLS + 2 * threadIdx.x;  // first of my two columns (0-based)
+  const long long j0 = rb * R;                                  // first interior row (0-based)
+  const bool v0 = i < nx, v1 = i + 1 < nx;          // my columns are interior
+  const bool l0 = i <= nx, l1 = i + 1 <= nx;        // ... or interior / east ring (loadable)
+  T x0[R + 2], x1[R + 2];
+  T f0[R], f1[R];
+#pragma unroll
+  for (int r = 0; r < R + 2; ++r) {            // padded rows j0 .. j0+R+1
+    const long long pj = j0 + r;
+    x0[r] = x1[r] = T(0);
+    if (pj <= ny + 1) {
+      const T* p = xin + pj * pitch + COL0 + i;
+      if (l1) {
+        const auto v = *reinterpret_cast<const typename VecOf<T>::v2*>(p);
+        x0[r] = v.x;
+        x1[r] = v.y;
+      } else if (l0) {
+        x0[r] = p[0];
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const long long j = j0 + r;
+    f0[r] = f1[r] = T(0);
+    if (j < ny && v0) {
+      const T* p = h2f + j * fpitch + i;
+      if (v1) {
+        const auto v = *reinterpret_cast<const typename VecOf<T>::v2*>(p);
+        f0[r] = v.x;
+        f1[r] = v.y;
+      } else {
+        f0[r] = p[0];
+      }
+    }
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int r = 1; r <= R; ++r) {
+    const long long j = j0 + r - 1;
+    T w = __shfl_up_sync(FULL, x1[r], 1);
+    T e = __shfl_down_sync(FULL, x0[r], 1);
+    if (lane == 0 && j < ny && v0) w = xin[(j + 1) * pitch + COL0 + i - 1];
+    if (lane == 31 && j < ny && v1) e = xin[(j + 1) * pitch + COL0 + i + 2];
+    if (j < ny) {
+      if (v0) {
+        const double s = res2((double)x0[r], (double)w, (double)x1[r], (double)x0[r - 1],
+                              (double)x0[r + 1], (double)f0[r - 1]);
+        acc = __fma_rn(s, s, acc);
+        if (write)
+          xout[(j + 1) * pitch + COL0 + i] = upd2(w, x1[r], x0[r - 1], x0[r + 1], qscale2<T>(f0[r - 1]));
+      }
+      if (v1) {
+        const double s = res2((double)x1[r], (double)x0[r], (double)e, (double)x1[r - 1],
+                              (double)x1[r + 1], (double)f1[r - 1]);
+        acc = __fma_rn(s, s, acc);
+        if (write)
+          xout[(j + 1) * pitch + COL0 + i + 1] =
+              upd2(x0[r], e, x1[r - 1], x1[r + 1], qscale2<T>(f1[r - 1]));
+      }
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) wsum[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) part[blockIdx.x] = ((wsum[0] + wsum[1]) + wsum[2]) + wsum[3];
+}
+
+template <typename T>
+cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
+  if (g.kernel_kind == K_REG2D) {
+    using C = R2<T>;
+    long long ctas = (g.ntiles + C::WARPS - 1) / C::WARPS;
+    if (ctas > grid_hint) ctas = grid_hint;
+    reg2d_kernel<T><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
+        *a.tm_in, *a.tm_f, (T*)a.xout, g.pitch, (int)g.nx, (int)g.ny, (int)g.ntx, g.ntiles, a.part,
+        a.ctrl, g.k, a.max_cycles);
+  } else if (g.kernel_kind == K_SMEM2D) {
+    const size_t smem = sizeof(T) * (2 * size_t(g.tx + 2) * (g.ty + 2) + size_t(g.tx) * g.ty);
+    smem2d_kernel<T><<<(unsigned)g.ntiles, dim3(g.tx, g.ty), smem, st>>>(
+        (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
+        (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles);
+  } else {
+    classic2d_kernel<T><<<(unsigned)g.ntiles, 128, 0, st>>>(
+        (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
+        (int)g.ntx, a.part, a.ctrl, a.max_cycles);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t reg2d_smem_bytes(int dtype) { return dtype == HJ_F64 ? R2<double>::SMEM : R2<float>::SMEM; }
+int reg2d_warps_per_cta(int dtype) { return dtype == HJ_F64 ? R2<double>::WARPS : R2<float>::WARPS; }
+
+cudaError_t configure_2d() {
+  cudaError_t e;
+  e = cudaFuncSetAttribute(reg2d_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)R2<double>::SMEM);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(reg2d_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)R2<float>::SMEM);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(smem2d_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(smem2d_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+cudaError_t launch_cycle_2d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
+  return g.dtype == HJ_F64 ? launch_2d_t<double>(g, a, grid_hint, st)
+                           : launch_2d_t<float>(g, a, grid_hint, st);
+}
+
+}  // namespace hj
