@@ -173,16 +173,16 @@ def main():
     n, k = args.n, (args.k if args.mode == "hier" else 1)
     h = 1.0 / (n + 1)
     # row slab of this rank (whole tile rows; PAPER-faithful tiles never straddle ranks)
-    unit = TILE if args.mode == "hier" else 16
-    rows_units = (n + unit - 1) // unit
-    rb = (rows_units * rank // world) * unit
-    re = min((rows_units * (rank + 1) // world) * unit, n)
+    from paper_2006_16465_b200.slabs import slab
+    rb, re = slab(n, TILE if args.mode == "hier" else 16, rank, world)
     nloc = re - rb
     f = torch.ones(nloc * n, dtype=torch.float64, device=dev)     # protocol P
     x0 = torch.ones(nloc * n, dtype=torch.float64, device=dev)
     bc = torch.zeros(4 * n, dtype=torch.float64, device=dev)
     prm = dict(mode=args.mode, tile=(TILE, TILE), k=k, tol=0.0, max_cycles=1 << 62, kernel=args.kernel)
-    stream = torch.cuda.current_stream(dev).cuda_stream
+    sobj = torch.cuda.Stream(dev)          # the plan's stream: graphs and timing events live here
+    stream = sobj.cuda_stream
+    torch.cuda.synchronize()               # inputs were written on torch's stream
     if world > 1:
         idb = [hj.hj_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(idb, src=0)
@@ -204,9 +204,9 @@ def main():
     with ClockSampler(local) as clk:
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        e0.record(sobj)
         kernel_ms = plan.run(args.steps, timed=True)   # events around each cycle kernel, on its stream
-        e1.record()
+        e1.record(sobj)
         barrier()
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms, kernel_ms], dtype=torch.float64, device=dev)

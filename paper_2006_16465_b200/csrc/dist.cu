@@ -10,13 +10,49 @@
 //   residual:  ncclAllReduce(sum) of the per-tile-row partial vector; each rank contributes only
 //              its own tile rows (zeros elsewhere), so the sum is exact and order-independent.
 // All calls are on the plan's stream and are captured in the cycle graph.
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "hj_internal.cuh"
 #include "hj_plan.h"
+
+// NCCL is resolved at run time (dlopen) rather than linked: the process may already hold
+// torch's bundled libnccl.so.2, and binding the system copy first would break it.  RTLD_NOLOAD
+// reuses an already-loaded libnccl.so.2; otherwise the default search path is used.
+namespace {
+struct NcclApi {
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  bool ok = false;
+  std::string err;
+};
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) { api.err = dlerror(); return; }
+#define HJ_SYM(name) api.name = reinterpret_cast<decltype(api.name)>(dlsym(h, "nccl" #name)); if (!api.name) { api.err = "missing nccl" #name; return; }
+    HJ_SYM(GetUniqueId) HJ_SYM(CommInitRank) HJ_SYM(CommDestroy) HJ_SYM(Send) HJ_SYM(Recv)
+    HJ_SYM(GroupStart) HJ_SYM(GroupEnd) HJ_SYM(AllReduce) HJ_SYM(GetErrorString)
+#undef HJ_SYM
+    api.ok = true;
+  });
+  return api;
+}
+}  // namespace
 
 struct DistState {
   ncclComm_t comm = nullptr;
@@ -27,9 +63,13 @@ namespace hj {
 
 #define HJ_NCCL(call)                                                                     \
   do {                                                                                    \
-    ncclResult_t r_ = (call);                                                             \
+    if (!nccl().ok) {                                                                     \
+      set_error("libnccl.so.2 unavailable: " + nccl().err);                             \
+      return HJ_ERR_NCCL;                                                                 \
+    }                                                                                     \
+    ncclResult_t r_ = (nccl().call);                                                      \
     if (r_ != ncclSuccess) {                                                              \
-      set_error(std::string(#call) + ": " + ncclGetErrorString(r_));                     \
+      set_error(std::string(#call) + ": " + nccl().GetErrorString(r_));                  \
       return HJ_ERR_NCCL;                                                                 \
     }                                                                                     \
   } while (0)
@@ -62,7 +102,7 @@ hj_status dist_create(hj_plan* P, const DistInfo* di) {
   P->dist = d;
   ncclUniqueId id;
   std::memcpy(&id, di->nccl_id, sizeof(id));
-  HJ_NCCL(ncclCommInitRank(&d->comm, di->nranks, id, di->rank));
+  HJ_NCCL(CommInitRank(&d->comm, di->nranks, id, di->rank));
   return HJ_OK;
 }
 
@@ -75,16 +115,16 @@ hj_status dist_halo_exchange(hj_plan* P, int buf) {
   char* X = static_cast<char*>(P->X[buf]);
   auto row = [&](long long r) { return X + (size_t(r) * g.pitch + g.col0) * esz; };
   const long long R = g.ny;
-  HJ_NCCL(ncclGroupStart());
+  HJ_NCCL(GroupStart());
   if (d->rank > 0) {
-    HJ_NCCL(ncclSend(row(1), g.nx, ty, d->rank - 1, d->comm, P->stream));
-    HJ_NCCL(ncclRecv(row(0), g.nx, ty, d->rank - 1, d->comm, P->stream));
+    HJ_NCCL(Send(row(1), g.nx, ty, d->rank - 1, d->comm, P->stream));
+    HJ_NCCL(Recv(row(0), g.nx, ty, d->rank - 1, d->comm, P->stream));
   }
   if (d->rank < d->nranks - 1) {
-    HJ_NCCL(ncclSend(row(R), g.nx, ty, d->rank + 1, d->comm, P->stream));
-    HJ_NCCL(ncclRecv(row(R + 1), g.nx, ty, d->rank + 1, d->comm, P->stream));
+    HJ_NCCL(Send(row(R), g.nx, ty, d->rank + 1, d->comm, P->stream));
+    HJ_NCCL(Recv(row(R + 1), g.nx, ty, d->rank + 1, d->comm, P->stream));
   }
-  HJ_NCCL(ncclGroupEnd());
+  HJ_NCCL(GroupEnd());
   return HJ_OK;
 }
 
@@ -97,14 +137,14 @@ hj_status dist_allreduce(hj_plan* P) {
                             cudaMemcpyDeviceToDevice, P->stream));
     return HJ_OK;
   }
-  HJ_NCCL(ncclAllReduce(P->rowpart_local, P->rowpart, P->g.nrg_global, ncclFloat64, ncclSum, d->comm,
+  HJ_NCCL(AllReduce(P->rowpart_local, P->rowpart, P->g.nrg_global, ncclFloat64, ncclSum, d->comm,
                         P->stream));
   return HJ_OK;
 }
 
 void dist_free(hj_plan* P) {
   if (!P->dist) return;
-  if (P->dist->comm) ncclCommDestroy(P->dist->comm);
+  if (P->dist->comm && nccl().ok) nccl().CommDestroy(P->dist->comm);
   delete P->dist;
   P->dist = nullptr;
 }
@@ -118,7 +158,7 @@ extern "C" {
 hj_status hj_nccl_unique_id(char out[128]) {
   if (!out) { set_error("NULL out"); return HJ_ERR_INVALID_ARG; }
   ncclUniqueId id;
-  HJ_NCCL(ncclGetUniqueId(&id));
+  HJ_NCCL(GetUniqueId(&id));
   static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
   std::memcpy(out, &id, 128);
   return HJ_OK;

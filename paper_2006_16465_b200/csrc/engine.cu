@@ -334,6 +334,18 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
     g.fpitch = round_up(span + 64, 128 / esz);
     g.frows = 1;
   }
+  if (st == nullptr) {
+    // The legacy default stream cannot be captured into graphs: run the plan on its own
+    // stream, ordered after all prior work on the device (inputs may still be in flight).
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      set_error(std::string("plan stream: ") + cudaGetErrorString(e));
+      delete P;
+      return HJ_ERR_CUDA;
+    }
+    P->own_stream = true;
+  }
   P->stream = st;
   P->ny_global = ny_global;
   P->gy0 = gy0;
@@ -602,6 +614,10 @@ void plan_free(hj_plan* P) {
   cudaFree(P->x0_d);
   if (P->ctrl_h) cudaFreeHost(P->ctrl_h);
   for (auto ev : P->evpool) cudaEventDestroy(ev);
+  if (P->own_stream) {
+    cudaStreamSynchronize(P->stream);
+    cudaStreamDestroy(P->stream);
+  }
   if (P->ev0) cudaEventDestroy(P->ev0);
   if (P->ev1) cudaEventDestroy(P->ev1);
   delete P;

@@ -26,6 +26,7 @@ struct hj_plan {
   hj_params prm{};
   int nsm = 0;
   cudaStream_t stream = nullptr;
+  bool own_stream = false;           // created because the caller passed the NULL stream
   long long ny_global = 0, gy0 = 0;
   void* X[2] = {nullptr, nullptr};
   void* H2F = nullptr;

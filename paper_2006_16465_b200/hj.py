@@ -212,6 +212,7 @@ class Plan:
         self.dim, self.nx, self.ny = dim, nx, ny
         self._keep = (f, bc, x0)
         self.stream = stream if stream is not None else torch.cuda.current_stream(f.device).cuda_stream
+        torch.cuda.synchronize(f.device)   # inputs may have been written on another stream
         pb = hj_problem(dim, nx, ny, float(h), _dptr(f), _dptr(bc), _dptr(x0))
         self._p = _P()
         self._create(pb)
