@@ -404,6 +404,8 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
     for (int b = 0; b < 2; ++b) {
       s = make_tmap(&P->tmX[b], P->X[b], g.dtype, (u64)g.pitch, (u64)g.rows, (u64)g.pitch * esz, bw, 34);
       if (s != HJ_OK) return fail(s);
+      s = make_tmap(&P->tmXs[b], P->X[b], g.dtype, (u64)g.pitch, (u64)g.rows, (u64)g.pitch * esz, 32, 32);
+      if (s != HJ_OK) return fail(s);
     }
     s = make_tmap(&P->tmF, P->H2F, g.dtype, (u64)g.fpitch, (u64)g.frows, (u64)g.fpitch * esz, 32, 32);
     if (s != HJ_OK) return fail(s);
@@ -440,7 +442,15 @@ hj_status plan_reset(hj_plan* P) {
   return HJ_OK;
 }
 
-int launches_per_cycle(const hj_plan* P) { return P->dist ? 3 : 3; }
+int launches_per_cycle(const hj_plan* P) {
+  const Geom& g = P->g;
+  int n = 3;  // cycle kernel + rowsum + finalize
+  if (g.kernel_kind == K_REG2D) {
+    const long long nfull = (g.nx / 32) * (g.ny / 32);
+    n = (nfull > 0 ? 1 : 0) + (g.ntiles > nfull ? 1 : 0) + 2;
+  }
+  return n;
+}
 
 // One cycle with static parity p: X[p] -> X[p^1].
 hj_status launch_cycle(hj_plan* P, int p, bool timed, float* acc_ms) {
@@ -452,6 +462,7 @@ hj_status launch_cycle(hj_plan* P, int p, bool timed, float* acc_ms) {
   a.h2f = P->H2F;
   a.tm_in = &P->tmX[p];
   a.tm_f = &P->tmF;
+  a.tm_out = &P->tmXs[p ^ 1];
   a.part = P->part;
   a.ctrl = P->ctrl;
   a.max_cycles = P->prm.max_cycles;

@@ -66,8 +66,9 @@ struct CycleArgs {
   const void* xin;
   void* xout;
   const void* h2f;
-  const CUtensorMap* tm_in;   // TMA descriptor of xin (REG2D)
-  const CUtensorMap* tm_f;    // TMA descriptor of h2f (REG2D)
+  const CUtensorMap* tm_in;   // TMA descriptor of xin, 34 x (col0+34) box (REG2D loads)
+  const CUtensorMap* tm_f;    // TMA descriptor of h2f, 32 x 32 box (REG2D loads)
+  const CUtensorMap* tm_out;  // TMA descriptor of xout, 32 x 32 box (REG2D stores)
   double* part;               // per-tile residual partials of the snapshot
   const Ctrl* ctrl;
   long long max_cycles;
@@ -132,6 +133,24 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// 2D tensor tile shared -> global (TMA store, SASS UTMASTG), tracked by bulk groups.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(tm)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the shared-memory sources of all committed bulk stores have been read
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// all committed bulk stores are complete (globally visible)
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// order this thread's generic-proxy shared-memory accesses before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* tm) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");

@@ -41,7 +41,8 @@ struct hj_plan {
   double* bc_d = nullptr;
   double* x0_d = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  CUtensorMap tmX[2];
+  CUtensorMap tmX[2];   // loads: 34-row box with halo
+  CUtensorMap tmXs[2];  // stores: 32x32 interior box
   CUtensorMap tmF;
   std::map<int, cudaGraphExec_t> graphs;
   long long c_host = 0;

@@ -21,10 +21,12 @@ template <> struct VecOf<float> { using v2 = float2; };
 // REG2D — the B200 design for 32x32 tiles.  One warp owns one tile; the tile lives in
 // registers: lane l holds rows 8*(l>>3)..+7 and columns 4*(l&7)..+3 of the interior
 // (32 cells), so a sub-iteration is 4 FP64 ops per cell plus warp shuffles for the
-// 4x8-lane block edges; the frozen halo sits in registers of the edge lanes.
-// Each warp double-buffers its next tiles in shared memory with TMA
-// (cp.async.bulk.tensor.2d, completion on a per-slot mbarrier), so HBM traffic for the
-// next tile overlaps the k sub-iterations of the current one.  Persistent grid.
+// 4x8-lane block edges.  Per warp, shared memory holds ONE input slot (x box with halo + h2f
+// box, filled by TMA and completed on an mbarrier), the frozen halo of the tile in flight and
+// an output staging tile drained by a TMA tensor store.  Registers are the second buffer:
+// as soon as a tile is in registers the slot is refilled with the warp's next tile, so its
+// HBM traffic overlaps the k sub-iterations.  Persistent grid, 4 warps per SM sub-partition
+// multiple (8 f64 / 12 f32 warps per CTA, one CTA per SM).
 // =============================================================================
 template <typename T>
 struct R2 {
@@ -34,41 +36,60 @@ struct R2 {
   static constexpr int XBYTES = BW * BH * sizeof(T);
   static constexpr int XSLOT = (XBYTES + 127) / 128 * 128;
   static constexpr int FBYTES = 32 * 32 * sizeof(T);
-  static constexpr int SLOT = XSLOT + FBYTES;
-  static constexpr int WARPS = sizeof(T) == 8 ? 6 : 12;
+  static constexpr int OBYTES = 32 * 32 * sizeof(T);                   // output staging tile
+  static constexpr int HALO = 128 * sizeof(T);                          // frozen halo W|E|S|N
+  static constexpr int WSMEM = XSLOT + FBYTES + OBYTES + HALO;          // per warp
+  static constexpr int WARPS = sizeof(T) == 8 ? 8 : 12;
   static constexpr int BARS = 128;                                      // barrier region bytes
-  static constexpr size_t SMEM = 128 + BARS + size_t(WARPS) * 2 * SLOT; // +128 for alignment
+  static constexpr size_t SMEM = 128 + BARS + size_t(WARPS) * WSMEM;    // +128 for alignment
 };
 
 template <typename T, bool RAGGED>
 struct Tile2 {
-  T x[8][4];   // current iterate
-  T q[8][4];   // 0.25 * h^2 f
-  T hx[8];     // frozen W halo (lx == 0) or E halo (lx == 7) of my 8 rows
-  T hy[4];     // frozen S halo (ly == 0) or N halo (ly == 3) of my 4 columns
-  uint32_t act; // RAGGED: bit 4*i+c set if cell (i, c) is inside the tile
+  T x[8][4];      // current iterate
+  T q[8][4];      // 0.25 * h^2 f
+  const T* hxp;   // per-warp smem: frozen W (lx == 0) / E (lx == 7) halo of my 8 rows
+  const T* hyp;   // per-warp smem: frozen S (ly == 0) / N (ly == 3) halo of my 4 columns
+  uint32_t act;   // RAGGED: bit 4*i+c set if cell (i, c) is inside the tile
 
   __device__ __forceinline__ bool on(int i, int c) const {
     return !RAGGED || ((act >> (4 * i + c)) & 1u);
   }
 
-  // Residual of the snapshot, s^2 summed over my cells (double).
-  __device__ __forceinline__ double residual(int lx, int ly) const {
-    T up[4], dn[4];
+  // N/S neighbour rows across lane rows: row 0 of the lane below is my row 7's N, row 7 of the
+  // lane above is my row 0's S; the edge lane rows take the frozen halo (predicated loads).
+  __device__ __forceinline__ void exchange_ns(int ly, T (&up)[4], T (&dn)[4]) const {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       up[c] = __shfl_down_sync(FULL, x[0][c], 8);
       dn[c] = __shfl_up_sync(FULL, x[7][c], 8);
-      if (ly == 3) up[c] = hy[c];
-      if (ly == 0) dn[c] = hy[c];
     }
+    // every lane's halo pointer is valid, so the loads are unconditional and only the
+    // choice is a select (no divergent branches in the sub-iteration loop)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const T hv = hyp[c];
+      up[c] = ly == 3 ? hv : up[c];
+      dn[c] = ly == 0 ? hv : dn[c];
+    }
+  }
+  __device__ __forceinline__ void exchange_we(int lx, int i, T& w, T& e) const {
+    w = __shfl_up_sync(FULL, x[i][3], 1, 8);
+    e = __shfl_down_sync(FULL, x[i][0], 1, 8);
+    const T hv = hxp[i];
+    w = lx == 0 ? hv : w;
+    e = lx == 7 ? hv : e;
+  }
+
+  // Residual of the snapshot, s^2 summed over my cells (double).
+  __device__ __forceinline__ double residual(int lx, int ly) const {
+    T up[4], dn[4];
+    exchange_ns(ly, up, dn);
     double acc = 0.0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      T w = __shfl_up_sync(FULL, x[i][3], 1, 8);
-      T e = __shfl_down_sync(FULL, x[i][0], 1, 8);
-      if (lx == 0) w = hx[i];
-      if (lx == 7) e = hx[i];
+      T w, e;
+      exchange_we(lx, i, w, e);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const T W = c == 0 ? w : x[i][c - 1];
@@ -85,26 +106,21 @@ struct Tile2 {
 
   // One Jacobi sub-iteration, rows processed top-down (DOWN) or bottom-up, keeping only
   // one saved old row; alternating directions lets the register allocator rotate names.
-  template <bool DOWN>
-  __device__ __forceinline__ void sweep(int lx, int ly) {
+  // RES (f64 only): also accumulate the snapshot residual from the same neighbour sums:
+  // s = h2f - (4x - ((W+E)+(S+N))) with h2f = 4q and 4x exact, so two fmas give the oracle's
+  // bits: t = fma(4, x, -sum) = 4x - sum,  s = fma(4, q, -t) = h2f - t.
+  template <bool DOWN, bool RES = false>
+  __device__ __forceinline__ void sweep(int lx, int ly, double* acc = nullptr) {
     T up[4], dn[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      up[c] = __shfl_down_sync(FULL, x[0][c], 8);   // row 0 of the lane below -> my N of row 7
-      dn[c] = __shfl_up_sync(FULL, x[7][c], 8);     // row 7 of the lane above -> my S of row 0
-      if (ly == 3) up[c] = hy[c];
-      if (ly == 0) dn[c] = hy[c];
-    }
+    exchange_ns(ly, up, dn);
     T saved[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) saved[c] = DOWN ? dn[c] : up[c];
 #pragma unroll
     for (int ii = 0; ii < 8; ++ii) {
       const int i = DOWN ? ii : 7 - ii;
-      T w = __shfl_up_sync(FULL, x[i][3], 1, 8);
-      T e = __shfl_down_sync(FULL, x[i][0], 1, 8);
-      if (lx == 0) w = hx[i];
-      if (lx == 7) e = hx[i];
+      T w, e;
+      exchange_we(lx, i, w, e);
       T nw[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -112,7 +128,15 @@ struct Tile2 {
         const T E = c == 3 ? e : x[i][c + 1];
         const T S = DOWN ? saved[c] : (i == 0 ? dn[c] : x[i - 1][c]);
         const T N = DOWN ? (i == 7 ? up[c] : x[i + 1][c]) : saved[c];
-        nw[c] = upd2(W, E, S, N, q[i][c]);
+        if constexpr (RES) {
+          const double sum = __dadd_rn(__dadd_rn(W, E), __dadd_rn(S, N));
+          nw[c] = __fma_rn(0.25, sum, q[i][c]);
+          const double t = __fma_rn(4.0, x[i][c], -sum);
+          const double r = __fma_rn(4.0, q[i][c], -t);
+          if (on(i, c)) *acc = __fma_rn(r, r, *acc);
+        } else {
+          nw[c] = upd2(W, E, S, N, q[i][c]);
+        }
       }
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -123,81 +147,80 @@ struct Tile2 {
   }
 };
 
-template <typename T, bool RAGGED>
+// One full 32x32 tile: smem slot -> registers, refill, fused residual, k sub-iterations, store.
+template <typename T, typename Refill, typename Store>
 __device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __restrict__ sf,
-                                           T* __restrict__ xout, long long pitch, long long tx,
-                                           long long ty, int w, int hgt, int lane, int kk,
-                                           double* __restrict__ part, long long t,
-                                           uint64_t* bar_reissue, const CUtensorMap* tmX,
-                                           const CUtensorMap* tmF, long long t_next, int ntx,
-                                           void* slot_x, void* slot_f) {
+                                           T* __restrict__ so, T* __restrict__ hb, int lane, int kk,
+                                           double* __restrict__ part, long long t, Refill&& refill,
+                                           Store&& store) {
   using C = R2<T>;
+  using V2 = typename VecOf<T>::v2;
   const int lx = lane & 7, ly = lane >> 3;
-  Tile2<T, RAGGED> tl;
-  // shared -> registers
+  Tile2<T, false> tl;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < 8; ++i) {  // 128-bit shared loads
     const int r = 8 * ly + i;
-    const T* rowx = sx + (r + 1) * C::BW + C::COL0 + 4 * lx;
-    const T* rowf = sf + r * 32 + 4 * lx;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      tl.x[i][c] = rowx[c];
-      tl.q[i][c] = qscale2<T>(rowf[c]);
-    }
-    tl.hx[i] = sx[(r + 1) * C::BW + (lx == 0 ? C::COL0 - 1 : C::COL0 + 32)];
+    const V2* rowx = reinterpret_cast<const V2*>(sx + (r + 1) * C::BW + C::COL0 + 4 * lx);
+    const V2* rowf = reinterpret_cast<const V2*>(sf + r * 32 + 4 * lx);
+    const V2 a = rowx[0], b = rowx[1], fa = rowf[0], fb = rowf[1];
+    tl.x[i][0] = a.x; tl.x[i][1] = a.y; tl.x[i][2] = b.x; tl.x[i][3] = b.y;
+    tl.q[i][0] = qscale2<T>(fa.x); tl.q[i][1] = qscale2<T>(fa.y);
+    tl.q[i][2] = qscale2<T>(fb.x); tl.q[i][3] = qscale2<T>(fb.y);
   }
-#pragma unroll
-  for (int c = 0; c < 4; ++c) tl.hy[c] = sx[(ly == 0 ? 0 : 33) * C::BW + C::COL0 + 4 * lx + c];
-  tl.act = 0;
-  if (RAGGED) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (8 * ly + i < hgt && 4 * lx + c < w) tl.act |= 1u << (4 * i + c);
-  }
-  // fused residual of the snapshot (consumes every loaded value)
-  double acc = warp_sum(tl.residual(lx, ly));
-  if (lane == 0) part[t] = acc;
+  // frozen halo -> the warp's halo buffer [W(32) | E(32) | S(32) | N(32)]
+  hb[lane] = sx[(lane + 1) * C::BW + C::COL0 - 1];
+  hb[32 + lane] = sx[(lane + 1) * C::BW + C::COL0 + 32];
+  hb[64 + lane] = sx[C::COL0 + lane];
+  hb[96 + lane] = sx[33 * C::BW + C::COL0 + lane];
+  tl.hxp = hb + (lx == 0 ? 0 : 32) + 8 * ly;
+  tl.hyp = hb + (ly == 0 ? 64 : 96) + 4 * lx;
+  tl.act = 0xffffffffu;
   __syncwarp();
-  // the slot is free: prefetch the tile after next into it
-  if (lane == 0 && t_next >= 0) {
-    const long long nx_ = t_next % ntx, ny_ = t_next / ntx;
-    mbar_arrive_expect_tx(bar_reissue, C::XBYTES + C::FBYTES);
-    tma_load_2d(slot_x, tmX, (int)(32 * nx_), (int)(32 * ny_), bar_reissue);
-    tma_load_2d(slot_f, tmF, (int)(32 * nx_), (int)(32 * ny_), bar_reissue);
-  }
-  // k sub-iterations, halo frozen
+  refill();  // every value of the slot is now in registers or the halo buffer
+  // fused residual of the snapshot: a separate pass for fp32 (residual in double, reading
+  // c16) and for residual-only cycles; fp64 folds it into the first sub-iteration below.
+  constexpr bool FOLD = sizeof(T) == 8;
+  double acc = 0.0;
+  if (!FOLD || kk == 0) acc = tl.residual(lx, ly);
   int s = 0;
+  if (FOLD && kk > 0) {
+    tl.template sweep<true, true>(lx, ly, &acc);
+    s = 1;
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) part[t] = acc;
+  // remaining sub-iterations, halo frozen; pairs of opposite-direction sweeps
+  if (s < kk && ((kk - s) & 1)) {
+    tl.template sweep<false>(lx, ly);
+    ++s;
+  }
 #pragma unroll 1
-  for (; s + 1 < kk; s += 2) {
+  for (; s < kk; s += 2) {
     tl.template sweep<true>(lx, ly);
     tl.template sweep<false>(lx, ly);
   }
-  if (s < kk) tl.template sweep<true>(lx, ly);
   if (kk == 0) return;  // residual-only pass (after max_cycles)
-  // registers -> global (interior of the NEXT iterate; snapshot semantics)
+  // registers -> staging tile -> TMA store into the NEXT iterate (snapshot semantics)
+  if (lane == 0) bulk_wait_read_all();  // the previous tile's store has read the staging tile
+  __syncwarp();
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const long long r = 32 * ty + 8 * ly + i;
-    T* dst = xout + (r + 1) * pitch + C::COL0 + 32 * tx + 4 * lx;
-    if (!RAGGED) {
-      using V2 = typename VecOf<T>::v2;
-      reinterpret_cast<V2*>(dst)[0] = V2{tl.x[i][0], tl.x[i][1]};
-      reinterpret_cast<V2*>(dst)[1] = V2{tl.x[i][2], tl.x[i][3]};
-    } else {
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (tl.on(i, c)) dst[c] = tl.x[i][c];
-    }
+    V2* dst = reinterpret_cast<V2*>(so + (8 * ly + i) * 32 + 4 * lx);
+    dst[0] = V2{tl.x[i][0], tl.x[i][1]};
+    dst[1] = V2{tl.x[i][2], tl.x[i][3]};
   }
+  fence_proxy_async();
+  __syncwarp();
+  store();
 }
 
+// Persistent kernel over the FULL 32x32 tiles (ntx_full x nty_full of them; ragged edge tiles,
+// if any, are done by smem2d_kernel in edge mode).  Warp w handles full tiles w, w+W, ...;
+// partials are indexed by the global tile index ty*ntx + tx.
 template <typename T>
 __global__ void __launch_bounds__(R2<T>::WARPS * 32, 1)
 reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
-             T* __restrict__ xout, long long pitch, int nx, int ny, int ntx, long long ntiles,
+             const __grid_constant__ CUtensorMap tmO, int ntx_full, long long nfull, int ntx,
              double* __restrict__ part, const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
   using C = R2<T>;
   if (ctrl->done) return;
@@ -206,46 +229,50 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base) + 2 * warp;
-  unsigned char* slot0 = base + C::BARS + size_t(warp) * 2 * C::SLOT;
-  unsigned char* slot1 = slot0 + C::SLOT;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base) + warp;
+  unsigned char* slot = base + C::BARS + size_t(warp) * C::WSMEM;
+  const T* sx = reinterpret_cast<const T*>(slot);
+  const T* sf = reinterpret_cast<const T*>(slot + C::XSLOT);
+  T* so = reinterpret_cast<T*>(slot + C::XSLOT + C::FBYTES);
+  T* hb = reinterpret_cast<T*>(slot + C::XSLOT + C::FBYTES + C::OBYTES);
   const long long gw = (long long)blockIdx.x * C::WARPS + warp;
   const long long nw = (long long)gridDim.x * C::WARPS;
-  if (gw >= ntiles) return;
+  if (gw >= nfull) return;
+  auto issue = [&](long long u) {  // u: full-tile index
+    const int cx = (int)(32 * (u % ntx_full)), cy = (int)(32 * (u / ntx_full));
+    mbar_arrive_expect_tx(bar, C::XBYTES + C::FBYTES);
+    tma_load_2d(slot, &tmX, cx, cy, bar);              // x box: padded rows 32ty.., cols 32tx..
+    tma_load_2d(slot + C::XSLOT, &tmF, cx, cy, bar);   // h2f box
+  };
   if (lane == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    mbar_init(bar, 1);
     fence_mbar_init();
     prefetch_tensormap(&tmX);
     prefetch_tensormap(&tmF);
-    for (int s = 0; s < 2; ++s) {
-      const long long t = gw + s * nw;
-      if (t < ntiles) {
-        unsigned char* sl = s ? slot1 : slot0;
-        mbar_arrive_expect_tx(&bars[s], C::XBYTES + C::FBYTES);
-        tma_load_2d(sl, &tmX, (int)(32 * (t % ntx)), (int)(32 * (t / ntx)), &bars[s]);
-        tma_load_2d(sl + C::XSLOT, &tmF, (int)(32 * (t % ntx)), (int)(32 * (t / ntx)), &bars[s]);
-      }
-    }
+    prefetch_tensormap(&tmO);
+    issue(gw);
   }
   __syncwarp();
   int it = 0;
-  for (long long t = gw; t < ntiles; t += nw, ++it) {
-    const int s = it & 1;
-    unsigned char* sl = s ? slot1 : slot0;
-    mbar_wait(&bars[s], (it >> 1) & 1);
-    const long long tx = t % ntx, ty = t / ntx;
-    const int w = (int)lmin(32, nx - 32 * tx), hgt = (int)lmin(32, ny - 32 * ty);
-    const long long tn = t + 2 * nw < ntiles ? t + 2 * nw : -1;
-    const T* sx = reinterpret_cast<const T*>(sl);
-    const T* sf = reinterpret_cast<const T*>(sl + C::XSLOT);
-    if (w == 32 && hgt == 32)
-      reg2d_tile<T, false>(sx, sf, xout, pitch, tx, ty, w, hgt, lane, kk, part, t, &bars[s], &tmX,
-                           &tmF, tn, ntx, sl, sl + C::XSLOT);
-    else
-      reg2d_tile<T, true>(sx, sf, xout, pitch, tx, ty, w, hgt, lane, kk, part, t, &bars[s], &tmX,
-                          &tmF, tn, ntx, sl, sl + C::XSLOT);
+  for (long long u = gw; u < nfull; u += nw, ++it) {
+    mbar_wait(bar, it & 1);
+    const long long tx = u % ntx_full, ty = u / ntx_full;
+    reg2d_tile<T>(
+        sx, sf, so, hb, lane, kk, part, ty * ntx + tx,
+        [&] {
+          if (lane == 0 && u + nw < nfull) {
+            fence_proxy_async();  // generic reads of the slot before the TMA overwrite
+            issue(u + nw);
+          }
+        },
+        [&] {
+          if (lane == 0) {
+            tma_store_2d(&tmO, (int)(C::COL0 + 32 * tx), (int)(32 * ty + 1), so);
+            bulk_commit();
+          }
+        });
   }
+  if (lane == 0) bulk_wait_all();
 }
 
 // =============================================================================
@@ -254,10 +281,12 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
 // paper's byte formula), __syncthreads between sub-iterations.  Any tile shape with
 // Tx*Ty <= 1024.  Used for tile shapes REG2D does not cover and as the in-tile baseline.
 // =============================================================================
+// edge != 0: only the ragged edge tiles — blocks [0, nty) are the last tile column (if nx is
+// ragged), the following blocks the last tile row (if ny is ragged) — for REG2D grids.
 template <typename T>
 __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
                               const T* __restrict__ h2f, long long pitch, long long fpitch, int nx,
-                              int ny, int ntx, double* __restrict__ part,
+                              int ny, int ntx, int nty, int edge, double* __restrict__ part,
                               const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
@@ -268,8 +297,16 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
   T* B = A + L * (Ty + 2);
   T* rhs = B + L * (Ty + 2);
   __shared__ double wsum[32];
-  const long long t = blockIdx.x;
-  const long long tx = t % ntx, ty = t / ntx;
+  long long tx, ty;
+  if (!edge) {
+    tx = blockIdx.x % ntx;
+    ty = blockIdx.x / ntx;
+  } else {
+    const int ncol = (nx % Tx) ? nty : 0;  // ragged last column
+    if ((int)blockIdx.x < ncol) { tx = ntx - 1; ty = blockIdx.x; }
+    else { tx = blockIdx.x - ncol; ty = nty - 1; }
+  }
+  const long long t = ty * ntx + tx;
   const long long i0 = tx * Tx, j0 = ty * Ty;  // interior origin (0-based)
   const int w = (int)lmin(Tx, nx - i0), hgt = (int)lmin(Ty, ny - j0);
   const int tid = threadIdx.y * Tx + threadIdx.x, nth = Tx * Ty;
@@ -403,18 +440,26 @@ classic2d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __res
 
 template <typename T>
 cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
+  const size_t smem_paper = sizeof(T) * (2 * size_t(g.tx + 2) * (g.ty + 2) + size_t(g.tx) * g.ty);
   if (g.kernel_kind == K_REG2D) {
     using C = R2<T>;
-    long long ctas = (g.ntiles + C::WARPS - 1) / C::WARPS;
-    if (ctas > grid_hint) ctas = grid_hint;
-    reg2d_kernel<T><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
-        *a.tm_in, *a.tm_f, (T*)a.xout, g.pitch, (int)g.nx, (int)g.ny, (int)g.ntx, g.ntiles, a.part,
-        a.ctrl, g.k, a.max_cycles);
+    const long long ntx_full = g.nx / 32, nty_full = g.ny / 32, nfull = ntx_full * nty_full;
+    if (nfull > 0) {
+      long long ctas = (nfull + C::WARPS - 1) / C::WARPS;
+      if (ctas > grid_hint) ctas = grid_hint;
+      reg2d_kernel<T><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
+          *a.tm_in, *a.tm_f, *a.tm_out, (int)ntx_full, nfull, (int)g.ntx, a.part, a.ctrl, g.k,
+          a.max_cycles);
+    }
+    const long long nedge = g.ntiles - nfull;
+    if (nedge > 0)
+      smem2d_kernel<T><<<(unsigned)nedge, dim3(32, 32), smem_paper, st>>>(
+          (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
+          (int)g.ntx, (int)g.nty, 1, a.part, a.ctrl, g.k, a.max_cycles);
   } else if (g.kernel_kind == K_SMEM2D) {
-    const size_t smem = sizeof(T) * (2 * size_t(g.tx + 2) * (g.ty + 2) + size_t(g.tx) * g.ty);
-    smem2d_kernel<T><<<(unsigned)g.ntiles, dim3(g.tx, g.ty), smem, st>>>(
+    smem2d_kernel<T><<<(unsigned)g.ntiles, dim3(g.tx, g.ty), smem_paper, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
-        (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles);
+        (int)g.ntx, (int)g.nty, 0, a.part, a.ctrl, g.k, a.max_cycles);
   } else {
     classic2d_kernel<T><<<(unsigned)g.ntiles, 128, 0, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
