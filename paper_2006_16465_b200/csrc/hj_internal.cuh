@@ -53,6 +53,7 @@ struct Geom {
   int64_t pitch, col0, rows; // X layout (elements)
   int64_t fpitch, frows;     // H2F layout: H2F[j*fpitch + i]
   int tx, ty, k;
+  int variant;                 // REG2D kernel variant (tuning knob, HJ_REG2D_VARIANT)
   int64_t ntx, nty, ntiles;  // tiles of this plan (classic: row-blocks x col-blocks)
   int64_t parts_per_row;     // partials per row group (= ntx)
   int64_t nrg_local, rg_offset, nrg_global;  // row groups (tile rows) and their global offset
@@ -77,8 +78,6 @@ struct CycleArgs {
 // Launchers (kernels_2d.cu / kernels_1d.cu).  Return cudaGetLastError().
 cudaError_t launch_cycle_2d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st);
 cudaError_t launch_cycle_1d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st);
-size_t reg2d_smem_bytes(int dtype);
-int reg2d_warps_per_cta(int dtype);
 size_t reg1d_smem_bytes(int dtype, int tile);
 int reg1d_warps_per_cta(int dtype, int tile);
 cudaError_t reg_kernels_configure();  // opt in to large dynamic shared memory

@@ -28,7 +28,7 @@ template <> struct VecOf<float> { using v2 = float2; };
 // HBM traffic overlaps the k sub-iterations.  Persistent grid, 4 warps per SM sub-partition
 // multiple (8 f64 / 12 f32 warps per CTA, one CTA per SM).
 // =============================================================================
-template <typename T>
+template <typename T, int WARPS_ = (sizeof(T) == 8 ? 8 : 12), bool TMA_STORE_ = true>
 struct R2 {
   static constexpr int COL0 = 16 / sizeof(T);                          // interior column offset
   static constexpr int BW = ((COL0 + 33) + (16 / sizeof(T)) - 1) / (16 / sizeof(T)) * (16 / sizeof(T));
@@ -36,12 +36,14 @@ struct R2 {
   static constexpr int XBYTES = BW * BH * sizeof(T);
   static constexpr int XSLOT = (XBYTES + 127) / 128 * 128;
   static constexpr int FBYTES = 32 * 32 * sizeof(T);
-  static constexpr int OBYTES = 32 * 32 * sizeof(T);                   // output staging tile
+  static constexpr bool TMA_STORE = TMA_STORE_;
+  static constexpr int OBYTES = TMA_STORE ? 32 * 32 * sizeof(T) : 0;   // output staging tile
   static constexpr int HALO = 128 * sizeof(T);                          // frozen halo W|E|S|N
   static constexpr int WSMEM = XSLOT + FBYTES + OBYTES + HALO;          // per warp
-  static constexpr int WARPS = sizeof(T) == 8 ? 8 : 12;
+  static constexpr int WARPS = WARPS_;
   static constexpr int BARS = 128;                                      // barrier region bytes
   static constexpr size_t SMEM = 128 + BARS + size_t(WARPS) * WSMEM;    // +128 for alignment
+  static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 template <typename T, bool RAGGED>
@@ -148,12 +150,11 @@ struct Tile2 {
 };
 
 // One full 32x32 tile: smem slot -> registers, refill, fused residual, k sub-iterations, store.
-template <typename T, typename Refill, typename Store>
+template <typename T, typename C, typename Refill, typename Store>
 __device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __restrict__ sf,
                                            T* __restrict__ so, T* __restrict__ hb, int lane, int kk,
                                            double* __restrict__ part, long long t, Refill&& refill,
-                                           Store&& store) {
-  using C = R2<T>;
+                                           Store&& store, T* __restrict__ gdst, long long pitch) {
   using V2 = typename VecOf<T>::v2;
   const int lx = lane & 7, ly = lane >> 3;
   Tile2<T, false> tl;
@@ -200,29 +201,39 @@ __device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __
     tl.template sweep<false>(lx, ly);
   }
   if (kk == 0) return;  // residual-only pass (after max_cycles)
-  // registers -> staging tile -> TMA store into the NEXT iterate (snapshot semantics)
-  if (lane == 0) bulk_wait_read_all();  // the previous tile's store has read the staging tile
-  __syncwarp();
+  if constexpr (C::TMA_STORE) {
+    // registers -> staging tile -> TMA store into the NEXT iterate (snapshot semantics)
+    if (lane == 0) bulk_wait_read_all();  // the previous tile's store has read the staging tile
+    __syncwarp();
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    V2* dst = reinterpret_cast<V2*>(so + (8 * ly + i) * 32 + 4 * lx);
-    dst[0] = V2{tl.x[i][0], tl.x[i][1]};
-    dst[1] = V2{tl.x[i][2], tl.x[i][3]};
+    for (int i = 0; i < 8; ++i) {
+      V2* dst = reinterpret_cast<V2*>(so + (8 * ly + i) * 32 + 4 * lx);
+      dst[0] = V2{tl.x[i][0], tl.x[i][1]};
+      dst[1] = V2{tl.x[i][2], tl.x[i][3]};
+    }
+    fence_proxy_async();
+    __syncwarp();
+    store();
+  } else {
+    // registers -> global, 128-bit stores (gdst = interior origin of the tile in the NEXT iterate)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      V2* dst = reinterpret_cast<V2*>(gdst + (8 * ly + i) * pitch + 4 * lx);
+      dst[0] = V2{tl.x[i][0], tl.x[i][1]};
+      dst[1] = V2{tl.x[i][2], tl.x[i][3]};
+    }
   }
-  fence_proxy_async();
-  __syncwarp();
-  store();
 }
 
 // Persistent kernel over the FULL 32x32 tiles (ntx_full x nty_full of them; ragged edge tiles,
 // if any, are done by smem2d_kernel in edge mode).  Warp w handles full tiles w, w+W, ...;
 // partials are indexed by the global tile index ty*ntx + tx.
-template <typename T>
-__global__ void __launch_bounds__(R2<T>::WARPS * 32, 1)
+template <typename T, typename C>
+__global__ void __launch_bounds__(C::WARPS * 32, 1)
 reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
-             const __grid_constant__ CUtensorMap tmO, int ntx_full, long long nfull, int ntx,
-             double* __restrict__ part, const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
-  using C = R2<T>;
+             const __grid_constant__ CUtensorMap tmO, T* __restrict__ xout, long long pitch,
+             int ntx_full, long long nfull, int ntx, double* __restrict__ part,
+             const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
   extern __shared__ unsigned char smem_raw[];
@@ -257,7 +268,7 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
   for (long long u = gw; u < nfull; u += nw, ++it) {
     mbar_wait(bar, it & 1);
     const long long tx = u % ntx_full, ty = u / ntx_full;
-    reg2d_tile<T>(
+    reg2d_tile<T, C>(
         sx, sf, so, hb, lane, kk, part, ty * ntx + tx,
         [&] {
           if (lane == 0 && u + nw < nfull) {
@@ -270,9 +281,10 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
             tma_store_2d(&tmO, (int)(C::COL0 + 32 * tx), (int)(32 * ty + 1), so);
             bulk_commit();
           }
-        });
+        },
+        xout + (32 * ty + 1) * pitch + C::COL0 + 32 * tx, pitch);
   }
-  if (lane == 0) bulk_wait_all();
+  if (C::TMA_STORE && lane == 0) bulk_wait_all();
 }
 
 // =============================================================================
@@ -442,14 +454,18 @@ template <typename T>
 cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
   const size_t smem_paper = sizeof(T) * (2 * size_t(g.tx + 2) * (g.ty + 2) + size_t(g.tx) * g.ty);
   if (g.kernel_kind == K_REG2D) {
-    using C = R2<T>;
     const long long ntx_full = g.nx / 32, nty_full = g.ny / 32, nfull = ntx_full * nty_full;
     if (nfull > 0) {
-      long long ctas = (nfull + C::WARPS - 1) / C::WARPS;
-      if (ctas > grid_hint) ctas = grid_hint;
-      reg2d_kernel<T><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
-          *a.tm_in, *a.tm_f, *a.tm_out, (int)ntx_full, nfull, (int)g.ntx, a.part, a.ctrl, g.k,
-          a.max_cycles);
+      auto go = [&](auto cfg) {
+        using C = decltype(cfg);
+        long long ctas = (nfull + C::WARPS - 1) / C::WARPS;
+        if (ctas > grid_hint) ctas = grid_hint;
+        reg2d_kernel<T, C><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
+            *a.tm_in, *a.tm_f, *a.tm_out, (T*)a.xout, g.pitch, (int)ntx_full, nfull, (int)g.ntx,
+            a.part, a.ctrl, g.k, a.max_cycles);
+      };
+      if (g.variant == 1 && sizeof(T) == 8) go(R2<T, 12, false>{});
+      else go(R2<T>{});
     }
     const long long nedge = g.ntiles - nfull;
     if (nedge > 0)
@@ -470,17 +486,17 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
 
 }  // namespace
 
-size_t reg2d_smem_bytes(int dtype) { return dtype == HJ_F64 ? R2<double>::SMEM : R2<float>::SMEM; }
-int reg2d_warps_per_cta(int dtype) { return dtype == HJ_F64 ? R2<double>::WARPS : R2<float>::WARPS; }
+
+template <typename T, typename C>
+cudaError_t cfg2() {
+  return cudaFuncSetAttribute(reg2d_kernel<T, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+}
 
 cudaError_t configure_2d() {
   cudaError_t e;
-  e = cudaFuncSetAttribute(reg2d_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)R2<double>::SMEM);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(reg2d_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)R2<float>::SMEM);
-  if (e != cudaSuccess) return e;
+  if ((e = cfg2<double, R2<double>>()) != cudaSuccess) return e;
+  if ((e = cfg2<double, R2<double, 12, false>>()) != cudaSuccess) return e;
+  if ((e = cfg2<float, R2<float>>()) != cudaSuccess) return e;
   e = cudaFuncSetAttribute(smem2d_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(smem2d_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
