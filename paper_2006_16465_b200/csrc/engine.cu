@@ -68,14 +68,17 @@ __global__ void init_x_kernel(T* __restrict__ X, long long pitch, long long rows
   }
 }
 
+// Q = scale * T(h^2 f), scale = 1/diag of the h^2-scaled stencil (0.5 in 1D, 0.25 in 2D): the
+// rhs term of the Jacobi update pre-divided by the diagonal.  Scaling by a
+// power of two is exact, so h^2 f = Q / scale exactly (the residual recovers it).
 template <typename T>
-__global__ void init_h2f_kernel(T* __restrict__ H, long long fpitch, long long frows, long long nx,
-                                long long ny, const double* __restrict__ f, double h2) {
+__global__ void init_q_kernel(T* __restrict__ Q, long long fpitch, long long frows, long long nx,
+                              long long ny, const double* __restrict__ f, double h2, T scale) {
   const long long n = fpitch * frows;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
        q += (long long)gridDim.x * blockDim.x) {
     const long long j = q / fpitch, i = q % fpitch;
-    H[q] = (i < nx && j < ny) ? (T)(h2 * f[j * nx + i]) : T(0);
+    Q[q] = (i < nx && j < ny) ? scale * (T)(h2 * f[j * nx + i]) : T(0);
   }
 }
 
@@ -294,6 +297,8 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
   g.ty = pr->mode == HJ_CLASSIC ? 1 : pr->tile_y;
   g.k = pr->mode == HJ_CLASSIC ? 1 : pr->k;
   if (const char* v = std::getenv("HJ_REG2D_VARIANT")) g.variant = std::atoi(v);
+  g.stagger_ns = 0;
+  if (const char* v = std::getenv("HJ_STAGGER_NS")) g.stagger_ns = std::atoi(v);
   hj_status s = choose_kernel(pb, pr, &g.kernel_kind);
   if (s != HJ_OK) { delete P; return s; }
   P->nsm = nsm;
@@ -394,10 +399,11 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
   PCK(cudaMemsetAsync(P->part, 0, sizeof(double) * (g.ntiles + 1), st));
   {
     const int blocks = 4 * nsm;
+    const double scale = g.dim == 2 ? 0.25 : 0.5;
     if (esz == 8)
-      init_h2f_kernel<double><<<blocks, 256, 0, st>>>((double*)P->H2F, g.fpitch, g.frows, g.nx, g.ny, pb->f, g.h2);
+      init_q_kernel<double><<<blocks, 256, 0, st>>>((double*)P->H2F, g.fpitch, g.frows, g.nx, g.ny, pb->f, g.h2, scale);
     else
-      init_h2f_kernel<float><<<blocks, 256, 0, st>>>((float*)P->H2F, g.fpitch, g.frows, g.nx, g.ny, pb->f, g.h2);
+      init_q_kernel<float><<<blocks, 256, 0, st>>>((float*)P->H2F, g.fpitch, g.frows, g.nx, g.ny, pb->f, g.h2, (float)scale);
     PCK(cudaGetLastError());
   }
   if (g.kernel_kind == K_REG2D) {

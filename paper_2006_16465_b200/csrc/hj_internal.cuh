@@ -54,6 +54,7 @@ struct Geom {
   int64_t fpitch, frows;     // H2F layout: H2F[j*fpitch + i]
   int tx, ty, k;
   int variant;                 // REG2D kernel variant (tuning knob, HJ_REG2D_VARIANT)
+  int stagger_ns;              // REG2D one-time per-warp start offset (HJ_STAGGER_NS)
   int64_t ntx, nty, ntiles;  // tiles of this plan (classic: row-blocks x col-blocks)
   int64_t parts_per_row;     // partials per row group (= ntx)
   int64_t nrg_local, rg_offset, nrg_global;  // row groups (tile rows) and their global offset
@@ -66,7 +67,7 @@ enum KernelKind { K_REG2D = 0, K_SMEM2D = 1, K_CLASSIC2D = 2, K_REG1D = 3, K_SME
 struct CycleArgs {
   const void* xin;
   void* xout;
-  const void* h2f;
+  const void* h2f;             // Q = T(h^2 f) / diag (0.25 in 2D, 0.5 in 1D), see init_q_kernel
   const CUtensorMap* tm_in;   // TMA descriptor of xin, 34 x (col0+34) box (REG2D loads)
   const CUtensorMap* tm_f;    // TMA descriptor of h2f, 32 x 32 box (REG2D loads)
   const CUtensorMap* tm_out;  // TMA descriptor of xout, 32 x 32 box (REG2D stores)
@@ -179,10 +180,6 @@ __device__ __forceinline__ double res2(double x, double w, double e, double s, d
 __device__ __forceinline__ double res1(double x, double l, double r, double h2f) {
   return h2f - (2.0 * x - (l + r));
 }
-template <typename T>
-__device__ __forceinline__ T qscale2(T h2f) { return T(0.25) * h2f; }
-template <typename T>
-__device__ __forceinline__ T qscale1(T h2f) { return T(0.5) * h2f; }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

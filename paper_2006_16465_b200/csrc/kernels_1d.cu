@@ -41,7 +41,7 @@ __device__ __forceinline__ void reg1d_tile(const T* __restrict__ sx, const T* __
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     x[c] = sx[P::COL0 + C * lane + c];
-    q[c] = qscale1<T>(sf[C * lane + c]);
+    q[c] = sf[C * lane + c];
   }
   const T hl = sx[P::COL0 - 1];       // frozen left halo (used by lane 0)
   const T hr = sx[P::COL0 + P::TILE]; // frozen right halo (used by lane 31) — for a ragged
@@ -180,7 +180,7 @@ __global__ void smem1d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
   __syncthreads();
   double s2 = 0.0;
   if (active) {
-    const double s = res1((double)A[a + 1], (double)A[a], (double)A[a + 2], (double)rhs[a]);
+    const double s = res1((double)A[a + 1], (double)A[a], (double)A[a + 2], (double)(T(2) * rhs[a]));
     s2 = s * s;
   }
   s2 = warp_sum(s2);
@@ -191,7 +191,7 @@ __global__ void smem1d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
     for (int q = 0; q < (Tn + 31) / 32; ++q) acc += wsum[q];
     part[t] = acc;
   }
-  const T q2 = active ? qscale1<T>(rhs[a]) : T(0);
+  const T q2 = active ? rhs[a] : T(0);
   T* cur = A;
   T* nxt = B;
   for (int s = 0; s < kk; ++s) {
@@ -235,9 +235,9 @@ classic1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __res
     const T L = c == 0 ? l : x[c - 1];
     const T R = c == V - 1 ? r : x[c + 1];
     if (i < nx) {
-      const double s = res1((double)x[c], (double)L, (double)R, (double)f[c]);
+      const double s = res1((double)x[c], (double)L, (double)R, (double)(T(2) * f[c]));
       acc = __fma_rn(s, s, acc);
-      if (write) xout[COL0 + i] = upd1(L, R, qscale1<T>(f[c]));
+      if (write) xout[COL0 + i] = upd1(L, R, f[c]);
     }
   }
   acc = warp_sum(acc);

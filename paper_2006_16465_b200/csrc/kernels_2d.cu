@@ -28,8 +28,9 @@ template <> struct VecOf<float> { using v2 = float2; };
 // HBM traffic overlaps the k sub-iterations.  Persistent grid, 4 warps per SM sub-partition
 // multiple (8 f64 / 12 f32 warps per CTA, one CTA per SM).
 // =============================================================================
-template <typename T, int WARPS_ = (sizeof(T) == 8 ? 8 : 12), bool TMA_STORE_ = true>
+template <typename T, int WARPS_ = (sizeof(T) == 8 ? 8 : 12), bool TMA_STORE_ = true, bool SAME_DIR_ = false>
 struct R2 {
+  static constexpr bool SAME_DIR = SAME_DIR_;
   static constexpr int COL0 = 16 / sizeof(T);                          // interior column offset
   static constexpr int BW = ((COL0 + 33) + (16 / sizeof(T)) - 1) / (16 / sizeof(T)) * (16 / sizeof(T));
   static constexpr int BH = 34;
@@ -112,7 +113,7 @@ struct Tile2 {
   // s = h2f - (4x - ((W+E)+(S+N))) with h2f = 4q and 4x exact, so two fmas give the oracle's
   // bits: t = fma(4, x, -sum) = 4x - sum,  s = fma(4, q, -t) = h2f - t.
   template <bool DOWN, bool RES = false>
-  __device__ __forceinline__ void sweep(int lx, int ly, double* acc = nullptr) {
+  __device__ __forceinline__ void sweep(int lx, int ly, double* acc = nullptr) {  // acc[4]
     T up[4], dn[4];
     exchange_ns(ly, up, dn);
     T saved[4];
@@ -135,7 +136,7 @@ struct Tile2 {
           nw[c] = __fma_rn(0.25, sum, q[i][c]);
           const double t = __fma_rn(4.0, x[i][c], -sum);
           const double r = __fma_rn(4.0, q[i][c], -t);
-          if (on(i, c)) *acc = __fma_rn(r, r, *acc);
+          if (on(i, c)) acc[c] = __fma_rn(r, r, acc[c]);
         } else {
           nw[c] = upd2(W, E, S, N, q[i][c]);
         }
@@ -165,8 +166,7 @@ __device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __
     const V2* rowf = reinterpret_cast<const V2*>(sf + r * 32 + 4 * lx);
     const V2 a = rowx[0], b = rowx[1], fa = rowf[0], fb = rowf[1];
     tl.x[i][0] = a.x; tl.x[i][1] = a.y; tl.x[i][2] = b.x; tl.x[i][3] = b.y;
-    tl.q[i][0] = qscale2<T>(fa.x); tl.q[i][1] = qscale2<T>(fa.y);
-    tl.q[i][2] = qscale2<T>(fb.x); tl.q[i][3] = qscale2<T>(fb.y);
+    tl.q[i][0] = fa.x; tl.q[i][1] = fa.y; tl.q[i][2] = fb.x; tl.q[i][3] = fb.y;
   }
   // frozen halo -> the warp's halo buffer [W(32) | E(32) | S(32) | N(32)]
   hb[lane] = sx[(lane + 1) * C::BW + C::COL0 - 1];
@@ -185,20 +185,28 @@ __device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __
   if (!FOLD || kk == 0) acc = tl.residual(lx, ly);
   int s = 0;
   if (FOLD && kk > 0) {
-    tl.template sweep<true, true>(lx, ly, &acc);
+    double a4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent accumulation chains
+    tl.template sweep<true, true>(lx, ly, a4);
+    acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
     s = 1;
   }
   acc = warp_sum(acc);
   if (lane == 0) part[t] = acc;
-  // remaining sub-iterations, halo frozen; pairs of opposite-direction sweeps
-  if (s < kk && ((kk - s) & 1)) {
-    tl.template sweep<false>(lx, ly);
-    ++s;
-  }
+  // remaining sub-iterations, halo frozen
+  if constexpr (C::SAME_DIR) {
 #pragma unroll 1
-  for (; s < kk; s += 2) {
-    tl.template sweep<true>(lx, ly);
-    tl.template sweep<false>(lx, ly);
+    for (; s < kk; ++s) tl.template sweep<true>(lx, ly);
+  } else {
+    // pairs of opposite-direction sweeps (register names rotate back after a pair)
+    if (s < kk && ((kk - s) & 1)) {
+      tl.template sweep<false>(lx, ly);
+      ++s;
+    }
+#pragma unroll 1
+    for (; s < kk; s += 2) {
+      tl.template sweep<true>(lx, ly);
+      tl.template sweep<false>(lx, ly);
+    }
   }
   if (kk == 0) return;  // residual-only pass (after max_cycles)
   if constexpr (C::TMA_STORE) {
@@ -233,7 +241,7 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
 reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
              const __grid_constant__ CUtensorMap tmO, T* __restrict__ xout, long long pitch,
              int ntx_full, long long nfull, int ntx, double* __restrict__ part,
-             const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
+             const Ctrl* __restrict__ ctrl, int k, long long max_cycles, int stagger_ns) {
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
   extern __shared__ unsigned char smem_raw[];
@@ -264,6 +272,10 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
     issue(gw);
   }
   __syncwarp();
+  // De-phase the warps of an SM once per launch: with fair bandwidth sharing, warps that start
+  // together receive their tiles together and stay phase-locked (memory bursts, then idle HBM
+  // while everyone computes).  A one-time offset of warp * stagger spreads the refills.
+  if (stagger_ns > 0 && warp > 0) __nanosleep((unsigned)(warp * stagger_ns));
   int it = 0;
   for (long long u = gw; u < nfull; u += nw, ++it) {
     mbar_wait(bar, it & 1);
@@ -340,7 +352,7 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
   const int c = (b + 1) * L + (a + 1);
   if (active) {
     const double s = res2((double)A[c], (double)A[c - 1], (double)A[c + 1], (double)A[c - L],
-                          (double)A[c + L], (double)rhs[b * Tx + a]);
+                          (double)A[c + L], (double)(T(4) * rhs[b * Tx + a]));
     s2 = s * s;
   }
   s2 = warp_sum(s2);
@@ -352,7 +364,7 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
     part[t] = acc;
   }
   // Step 2: k sub-iterations, ping-pong between the containers, halo frozen
-  const T q4 = active ? qscale2<T>(rhs[b * Tx + a]) : T(0);
+  const T q4 = active ? rhs[b * Tx + a] : T(0);
   T* cur = A;
   T* nxt = B;
   for (int s = 0; s < kk; ++s) {
@@ -429,18 +441,18 @@ classic2d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __res
     if (j < ny) {
       if (v0) {
         const double s = res2((double)x0[r], (double)w, (double)x1[r], (double)x0[r - 1],
-                              (double)x0[r + 1], (double)f0[r - 1]);
+                              (double)x0[r + 1], (double)(T(4) * f0[r - 1]));
         acc = __fma_rn(s, s, acc);
         if (write)
-          xout[(j + 1) * pitch + COL0 + i] = upd2(w, x1[r], x0[r - 1], x0[r + 1], qscale2<T>(f0[r - 1]));
+          xout[(j + 1) * pitch + COL0 + i] = upd2(w, x1[r], x0[r - 1], x0[r + 1], f0[r - 1]);
       }
       if (v1) {
         const double s = res2((double)x1[r], (double)x0[r], (double)e, (double)x1[r - 1],
-                              (double)x1[r + 1], (double)f1[r - 1]);
+                              (double)x1[r + 1], (double)(T(4) * f1[r - 1]));
         acc = __fma_rn(s, s, acc);
         if (write)
           xout[(j + 1) * pitch + COL0 + i + 1] =
-              upd2(x0[r], e, x1[r - 1], x1[r + 1], qscale2<T>(f1[r - 1]));
+              upd2(x0[r], e, x1[r - 1], x1[r + 1], f1[r - 1]);
       }
     }
   }
@@ -462,9 +474,9 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
         if (ctas > grid_hint) ctas = grid_hint;
         reg2d_kernel<T, C><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
             *a.tm_in, *a.tm_f, *a.tm_out, (T*)a.xout, g.pitch, (int)ntx_full, nfull, (int)g.ntx,
-            a.part, a.ctrl, g.k, a.max_cycles);
+            a.part, a.ctrl, g.k, a.max_cycles, g.stagger_ns);
       };
-      if (g.variant == 1 && sizeof(T) == 8) go(R2<T, 12, false>{});
+      if (g.variant == 2) go(R2<T, (sizeof(T) == 8 ? 8 : 12), true, true>{});
       else go(R2<T>{});
     }
     const long long nedge = g.ntiles - nfull;
@@ -495,7 +507,8 @@ cudaError_t cfg2() {
 cudaError_t configure_2d() {
   cudaError_t e;
   if ((e = cfg2<double, R2<double>>()) != cudaSuccess) return e;
-  if ((e = cfg2<double, R2<double, 12, false>>()) != cudaSuccess) return e;
+  if ((e = cfg2<double, R2<double, 8, true, true>>()) != cudaSuccess) return e;
+  if ((e = cfg2<float, R2<float, 12, true, true>>()) != cudaSuccess) return e;
   if ((e = cfg2<float, R2<float>>()) != cudaSuccess) return e;
   e = cudaFuncSetAttribute(smem2d_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return e;
