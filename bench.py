@@ -174,7 +174,7 @@ def main():
     h = 1.0 / (n + 1)
     # row slab of this rank (whole tile rows; PAPER-faithful tiles never straddle ranks)
     from paper_2006_16465_b200.slabs import slab
-    rb, re = slab(n, TILE if args.mode == "hier" else 16, rank, world)
+    rb, re = slab(n, TILE if args.mode == "hier" else 8, rank, world)
     nloc = re - rb
     f = torch.ones(nloc * n, dtype=torch.float64, device=dev)     # protocol P
     x0 = torch.ones(nloc * n, dtype=torch.float64, device=dev)

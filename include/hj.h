@@ -130,7 +130,7 @@ typedef struct {
   int32_t rank, nranks;
   const char *nccl_id;     /* 128 bytes from hj_nccl_unique_id() on rank 0, broadcast by caller */
   int64_t row_begin, row_end; /* this rank's interior rows [begin, end) of the global grid;
-                                 multiples of tile_y (hierarchical) / of 16 (classic)        */
+                                 multiples of tile_y (hierarchical) / of 8 (classic)        */
 } hj_dist;
 
 hj_status hj_nccl_unique_id(char out[128]);

@@ -326,7 +326,8 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
       g.ntx = (g.nx + CLASSIC1D_CELLS - 1) / CLASSIC1D_CELLS; g.nty = 1; g.nrg_global = 1; g.rg_offset = 0;
   }
   g.ntiles = g.ntx * g.nty;
-  g.parts_per_row = g.ntx;
+  g.parts_per_row = g.kernel_kind == K_CLASSIC2D ? 4 * g.ntx : g.ntx;
+  g.nparts = g.parts_per_row * g.nty;
   g.nrg_local = g.nty;
   // buffer geometry
   if (g.dim == 2) {
@@ -371,7 +372,7 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
   PCK(cudaMalloc(&P->X[0], xbytes));
   PCK(cudaMalloc(&P->X[1], xbytes));
   PCK(cudaMalloc(&P->H2F, fbytes));
-  PCK(cudaMalloc(&P->part, sizeof(double) * (g.ntiles + 1)));
+  PCK(cudaMalloc(&P->part, sizeof(double) * (g.nparts + 1)));
   PCK(cudaMalloc(&P->rowpart, sizeof(double) * (g.nrg_global + 1)));
   P->rowsum_dst = P->rowpart;
   if (di) {
@@ -396,7 +397,7 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
   if (pb->x0) PCK(cudaMemcpyAsync(P->x0_d, pb->x0, sizeof(double) * nloc, cudaMemcpyDefault, st));
   else PCK(cudaMemsetAsync(P->x0_d, 0, sizeof(double) * nloc, st));
   PCK(cudaMemsetAsync(P->rowpart, 0, sizeof(double) * (g.nrg_global + 1), st));
-  PCK(cudaMemsetAsync(P->part, 0, sizeof(double) * (g.ntiles + 1), st));
+  PCK(cudaMemsetAsync(P->part, 0, sizeof(double) * (g.nparts + 1), st));
   {
     const int blocks = 4 * nsm;
     const double scale = g.dim == 2 ? 0.25 : 0.5;

@@ -56,7 +56,8 @@ struct Geom {
   int variant;                 // REG2D kernel variant (tuning knob, HJ_REG2D_VARIANT)
   int stagger_ns;              // REG2D one-time per-warp start offset (HJ_STAGGER_NS)
   int64_t ntx, nty, ntiles;  // tiles of this plan (classic: row-blocks x col-blocks)
-  int64_t parts_per_row;     // partials per row group (= ntx)
+  int64_t parts_per_row;     // partials per row group (ntx; classic2d: 4 per CTA)
+  int64_t nparts;            // number of residual partials
   int64_t nrg_local, rg_offset, nrg_global;  // row groups (tile rows) and their global offset
   double h, h2;
 };
@@ -83,8 +84,8 @@ size_t reg1d_smem_bytes(int dtype, int tile);
 int reg1d_warps_per_cta(int dtype, int tile);
 cudaError_t reg_kernels_configure();  // opt in to large dynamic shared memory
 
-// Classic kernels block geometry (partials per 16-row x 256-col block).
-constexpr int CLASSIC2D_ROWS = 16;
+// Classic kernels block geometry (CTA = 8 rows x 256 cols, one residual partial per warp).
+constexpr int CLASSIC2D_ROWS = 8;
 constexpr int CLASSIC2D_COLS = 256;   // 128 threads x 2 columns
 constexpr int CLASSIC1D_CELLS = 2048; // 256 threads x 8 cells
 

@@ -148,6 +148,36 @@ struct Tile2 {
       }
     }
   }
+
+  // Ping-pong form: read src, write dst (no rolling row, no register renaming at the loop
+  // back-edge).  Used for the paired sub-iterations of the main loop.
+  __device__ __forceinline__ void sweep_pp(int lx, int ly, const T (&src)[8][4], T (&dst)[8][4]) const {
+    T up[4], dn[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      up[c] = __shfl_down_sync(FULL, src[0][c], 8);
+      dn[c] = __shfl_up_sync(FULL, src[7][c], 8);
+      const T hv = hyp[c];
+      up[c] = ly == 3 ? hv : up[c];
+      dn[c] = ly == 0 ? hv : dn[c];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      T w = __shfl_up_sync(FULL, src[i][3], 1, 8);
+      T e = __shfl_down_sync(FULL, src[i][0], 1, 8);
+      const T hv = hxp[i];
+      w = lx == 0 ? hv : w;
+      e = lx == 7 ? hv : e;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const T W = c == 0 ? w : src[i][c - 1];
+        const T E = c == 3 ? e : src[i][c + 1];
+        const T S = i == 0 ? dn[c] : src[i - 1][c];
+        const T N = i == 7 ? up[c] : src[i + 1][c];
+        dst[i][c] = upd2(W, E, S, N, q[i][c]);
+      }
+    }
+  }
 };
 
 // One full 32x32 tile: smem slot -> registers, refill, fused residual, k sub-iterations, store.
@@ -194,8 +224,17 @@ __device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __
   if (lane == 0) part[t] = acc;
   // remaining sub-iterations, halo frozen
   if constexpr (C::SAME_DIR) {
+    // register ping-pong: x -> y -> x per pair (variant 2)
+    if (s < kk && ((kk - s) & 1)) {
+      tl.template sweep<false>(lx, ly);
+      ++s;
+    }
+    T y[8][4];
 #pragma unroll 1
-    for (; s < kk; ++s) tl.template sweep<true>(lx, ly);
+    for (; s < kk; s += 2) {
+      tl.sweep_pp(lx, ly, tl.x, y);
+      tl.sweep_pp(lx, ly, y, tl.x);
+    }
   } else {
     // pairs of opposite-direction sweeps (register names rotate back after a pair)
     if (s < kk && ((kk - s) & 1)) {
@@ -378,20 +417,20 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
 
 // =============================================================================
 // CLASSIC2D — one Jacobi sweep over the grid, HBM-bound (24 B/cell f64):
-// a CTA of 128 threads covers 256 columns x 16 rows, each lane two adjacent columns with
-// 128-bit (f64) loads; W/E neighbours by warp shuffle, N/S from the 18 rows held in registers.
-// Fused residual of the snapshot, one partial per CTA.
+// a CTA of 128 threads covers 256 columns x CLASSIC2D_ROWS rows, each lane two adjacent columns
+// with 128-bit loads/stores; W/E neighbours by warp shuffle, N/S from the rows held in
+// registers.  Fused residual of the snapshot, one partial per WARP (no CTA barrier).
 // =============================================================================
 template <typename T>
 __global__ void __launch_bounds__(128)
-classic2d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restrict__ h2f,
+classic2d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restrict__ qarr,
                  long long pitch, long long fpitch, int nx, int ny, int ncb,
                  double* __restrict__ part, const Ctrl* __restrict__ ctrl, long long max_cycles) {
   if (ctrl->done) return;
   const bool write = ctrl->c < max_cycles;
   constexpr int COL0 = 16 / sizeof(T);
   constexpr int R = CLASSIC2D_ROWS;
-  __shared__ double wsum[4];
+  using V2 = typename VecOf<T>::v2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long cb = blockIdx.x % ncb, rb = blockIdx.x / ncb;
   const long long i = cb * CLASSIC2D_COLS + 2 * threadIdx.x;  // first of my two columns (0-based)
@@ -407,7 +446,7 @@ classic2d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __res
     if (pj <= ny + 1) {
       const T* p = xin + pj * pitch + COL0 + i;
       if (l1) {
-        const auto v = *reinterpret_cast<const typename VecOf<T>::v2*>(p);
+        const V2 v = *reinterpret_cast<const V2*>(p);
         x0[r] = v.x;
         x1[r] = v.y;
       } else if (l0) {
@@ -420,9 +459,9 @@ classic2d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __res
     const long long j = j0 + r;
     f0[r] = f1[r] = T(0);
     if (j < ny && v0) {
-      const T* p = h2f + j * fpitch + i;
+      const T* p = qarr + j * fpitch + i;
       if (v1) {
-        const auto v = *reinterpret_cast<const typename VecOf<T>::v2*>(p);
+        const V2 v = *reinterpret_cast<const V2*>(p);
         f0[r] = v.x;
         f1[r] = v.y;
       } else {
@@ -439,27 +478,28 @@ classic2d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __res
     if (lane == 0 && j < ny && v0) w = xin[(j + 1) * pitch + COL0 + i - 1];
     if (lane == 31 && j < ny && v1) e = xin[(j + 1) * pitch + COL0 + i + 2];
     if (j < ny) {
+      T n0 = T(0), n1 = T(0);
       if (v0) {
         const double s = res2((double)x0[r], (double)w, (double)x1[r], (double)x0[r - 1],
                               (double)x0[r + 1], (double)(T(4) * f0[r - 1]));
         acc = __fma_rn(s, s, acc);
-        if (write)
-          xout[(j + 1) * pitch + COL0 + i] = upd2(w, x1[r], x0[r - 1], x0[r + 1], f0[r - 1]);
+        n0 = upd2(w, x1[r], x0[r - 1], x0[r + 1], f0[r - 1]);
       }
       if (v1) {
         const double s = res2((double)x1[r], (double)x0[r], (double)e, (double)x1[r - 1],
                               (double)x1[r + 1], (double)(T(4) * f1[r - 1]));
         acc = __fma_rn(s, s, acc);
-        if (write)
-          xout[(j + 1) * pitch + COL0 + i + 1] =
-              upd2(x0[r], e, x1[r - 1], x1[r + 1], f1[r - 1]);
+        n1 = upd2(x0[r], e, x1[r - 1], x1[r + 1], f1[r - 1]);
+      }
+      if (write) {
+        T* dst = xout + (j + 1) * pitch + COL0 + i;
+        if (v1) *reinterpret_cast<V2*>(dst) = V2{n0, n1};
+        else if (v0) dst[0] = n0;
       }
     }
   }
   acc = warp_sum(acc);
-  if (lane == 0) wsum[warp] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) part[blockIdx.x] = ((wsum[0] + wsum[1]) + wsum[2]) + wsum[3];
+  if (lane == 0) part[(rb * ncb + cb) * 4 + warp] = acc;
 }
 
 template <typename T>
@@ -489,7 +529,7 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
         (int)g.ntx, (int)g.nty, 0, a.part, a.ctrl, g.k, a.max_cycles);
   } else {
-    classic2d_kernel<T><<<(unsigned)g.ntiles, 128, 0, st>>>(
+    classic2d_kernel<T><<<(unsigned)(g.ntx * g.nty), 128, 0, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
         (int)g.ntx, a.part, a.ctrl, a.max_cycles);
   }

@@ -1,0 +1,21 @@
+"""Small solves over every kernel family, for compute-sanitizer runs (no oracle; just exercise)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2006_16465_b200 import hj
+from paper_2006_16465_b200.inputs import make_problem
+
+cases = [
+    (2, 100, 70, dict(mode="hier", tile=(32, 32), k=5)),           # reg2d + ragged edge tiles
+    (2, 96, 64, dict(mode="hier", tile=(32, 32), k=4, dtype="f32")),
+    (2, 33, 40, dict(mode="hier", tile=(32, 32), k=3, kernel="smem")),
+    (2, 19, 13, dict(mode="hier", tile=(4, 5), k=7)),
+    (2, 300, 37, dict(mode="classic")),
+    (1, 5000, 1, dict(mode="hier", tile=128, k=7)),
+    (1, 1000, 1, dict(mode="hier", tile=96, k=5)),
+    (1, 5000, 1, dict(mode="classic")),
+]
+for dim, nx, ny, kw in cases:
+    p = make_problem("R", dim, nx, ny)
+    r = hj.jacobi_solve(dim, nx, ny, p["h"], p["f"], p["bc"], p["x0"], tol=1e-9, max_cycles=6, **kw)
+    print(dim, nx, ny, kw, "cycles", r["cycles"], "status", r["status"])
+print("sanitize cases done")
