@@ -52,13 +52,16 @@ def _load():
             d, i64, i32 = ctypes.c_double, ctypes.c_int64, ctypes.c_int
             P = ctypes.c_void_p
             lib.hjo_solve.restype = i32
-            lib.hjo_solve.argtypes = [i32, i64, i64, d, P, P, P, i32, i32, i64, i64, i32, d, i32, d,
-                                      i64, i32, P, P, ctypes.POINTER(i64), ctypes.POINTER(i32)]
+            lib.hjo_solve.argtypes = [i32, i64, i64, d, P, P, P, i32, i32, i64, i64, i64, i64, i32, d,
+                                      i32, d, i64, i32, P, P, ctypes.POINTER(i64), ctypes.POINTER(i32)]
+            lib.hjo_block_plan.restype = i64
+            lib.hjo_block_plan.argtypes = [i64, i64, i64, i64, P, P, P, P]
             lib.hjo_residual.restype = d
             lib.hjo_residual.argtypes = [i32, i64, i64, d, P, P, P]
             lib.hjo_resource_figures.restype = i32
-            lib.hjo_resource_figures.argtypes = [i32, i64, i64, i64, i64, i64, ctypes.POINTER(i64),
-                                                 ctypes.POINTER(i64), ctypes.POINTER(i64)]
+            lib.hjo_resource_figures.argtypes = [i32, i64, i64, i64, i64, i64, i64, i64,
+                                                 ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                                 ctypes.POINTER(i64)]
             _lib = lib
     return _lib
 
@@ -77,7 +80,7 @@ def _f64(a, n, name):
 
 
 def solve(dim, nx, ny, h, f, bc=None, x0=None, *, mode="hier", dtype="f64", tile=(32, 32), k=16,
-          tol=1e-4, tol_mode="rel", ref_residual=0.0, max_cycles=10**7, tile_order=0,
+          overlap=0, tol=1e-4, tol_mode="rel", ref_residual=0.0, max_cycles=10**7, tile_order=0,
           history=True):
     """Run the oracle solver.  Returns dict(x, history, cycles, converged, status).
 
@@ -96,8 +99,9 @@ def solve(dim, nx, ny, h, f, bc=None, x0=None, *, mode="hier", dtype="f64", tile
     cyc = ctypes.c_int64(0)
     conv = ctypes.c_int(0)
     tx, ty = (tile if isinstance(tile, (tuple, list)) else (tile, 1))
+    ox, oy = (overlap if isinstance(overlap, (tuple, list)) else (overlap, overlap if dim == 2 else 0))
     st = lib.hjo_solve(dim, nx, ny, float(h), _ptr(f), _ptr(bc), _ptr(x0),
-                       {"hier": 0, "classic": 1}[mode], {"f64": 0, "f32": 1}[dtype], tx, ty, k,
+                       {"hier": 0, "classic": 1}[mode], {"f64": 0, "f32": 1}[dtype], tx, ty, ox, oy, k,
                        float(tol), {"rel": 0, "abs": 1}[tol_mode], float(ref_residual),
                        int(max_cycles), int(tile_order), _ptr(x), _ptr(hist),
                        ctypes.byref(cyc), ctypes.byref(conv))
@@ -119,12 +123,24 @@ def residual(dim, nx, ny, h, f, bc, x):
     return lib.hjo_residual(dim, nx, ny, float(h), _ptr(f), _ptr(bc), _ptr(x))
 
 
-def resource_figures(dim, nx, ny, tx, ty=1, bytes_per_value=8):
+def resource_figures(dim, nx, ny, tx, ty=1, bytes_per_value=8, overlap=0):
     """(tiles, threads, shared bytes per block by the paper's formula)."""
     lib = _load()
+    ox, oy = (overlap if isinstance(overlap, (tuple, list)) else (overlap, overlap if dim == 2 else 0))
     a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-    st = lib.hjo_resource_figures(dim, nx, ny, tx, ty, bytes_per_value, ctypes.byref(a),
+    st = lib.hjo_resource_figures(dim, nx, ny, tx, ty, ox, oy, bytes_per_value, ctypes.byref(a),
                                   ctypes.byref(b), ctypes.byref(c))
     if st != 0:
         raise ValueError("oracle: invalid configuration")
     return a.value, b.value, c.value
+
+
+def block_plan(n, tile, overlap=0):
+    """Blocks of one dimension: list of (start, width, own_lo, own_hi), 1-based inclusive."""
+    lib = _load()
+    cap = n + 1
+    arrs = [np.zeros(cap, dtype=np.int64) for _ in range(4)]
+    nb = lib.hjo_block_plan(n, tile, overlap, cap, *[a.ctypes.data_as(ctypes.c_void_p) for a in arrs])
+    if nb < 0:
+        raise ValueError("oracle: invalid block plan")
+    return [tuple(int(a[b]) for a in arrs) for b in range(nb)]

@@ -27,6 +27,8 @@
 //   c8  the write-back takes the values after exactly k sub-iterations (odd k too);
 //   c10 ragged last tile when n is not a multiple of the tile;
 //   c12 the Dirichlet ring may hold non-zero values g;
+//   c21 overlapping subdomains: last block shifted left to end at n, half-split ownership with
+//       the left block taking the odd extra point (see block_plan);
 //   c3  the residual is computed in the h^2-scaled form
 //       s = h^2 f - (2x - (x_{i-1}+x_{i+1}))            (1D)
 //       s = h^2 f - (4x - ((xW+xE)+(xS+xN)))            (2D)
@@ -61,6 +63,50 @@
 #include <algorithm>
 
 namespace {
+
+// ------------------------------------------------------------ block plan -----
+// Subdomains along one dimension of n interior points (1-based), tile width T, overlap o.
+//  o = 0: tiles [1 + t*T, min((t+1)*T, n)], ragged last tile (reading c10);
+//        every tile owns its whole interior.
+//  o > 0 (PAPER.md:243-258, §3.5; :454-458, §4.3): block b starts at 1 + b*(T - o) and spans T
+//        points; the number of blocks is ceil((n - T)/(T - o)) + 1 (= (n - o)/(T - o) when it
+//        divides, Eq. 8); if it does not divide, the last block is shifted left to
+//        end at n (reading c21).  In each overlap between consecutive blocks the
+//        left block owns the left half and the right block the right half, the left block
+//        taking the extra point when the overlap is odd (reading c21).
+struct BlockPlan {
+  std::vector<int64_t> start, width, own_lo, own_hi;  // 1-based, inclusive
+};
+
+inline BlockPlan block_plan(int64_t n, int64_t T, int64_t o) {
+  BlockPlan P;
+  if (o == 0) {
+    for (int64_t s = 1; s <= n; s += T) {
+      const int64_t w = std::min(T, n - s + 1);
+      P.start.push_back(s);
+      P.width.push_back(w);
+      P.own_lo.push_back(s);
+      P.own_hi.push_back(s + w - 1);
+    }
+    return P;
+  }
+  const int64_t nb = (n - T + (T - o) - 1) / (T - o) + 1;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t s = (b == nb - 1) ? n - T + 1 : 1 + b * (T - o);
+    P.start.push_back(s);
+    P.width.push_back(T);
+  }
+  P.own_lo.assign(nb, 1);
+  P.own_hi.assign(nb, n);
+  for (int64_t b = 0; b + 1 < nb; ++b) {
+    const int64_t ov_lo = P.start[b + 1], ov_hi = P.start[b] + T - 1;  // overlap region
+    const int64_t L = ov_hi - ov_lo + 1;
+    const int64_t left_end = ov_lo + (L + 1) / 2 - 1;                  // left takes ceil(L/2)
+    P.own_hi[b] = left_end;
+    P.own_lo[b + 1] = left_end + 1;
+  }
+  return P;
+}
 
 // ---------------------------------------------------------------- 1D ----------
 
@@ -103,20 +149,19 @@ void classic_sweep_1d(const Problem1D<T>& p, const std::vector<T>& x0, std::vect
     x1[i] = update1d<T>(x0[i - 1], x0[i + 1], p.h2f[i - 1]);
 }
 
-// §3.3 hierarchical cycle, 1D (Appendix A :548-573), o = 0.
-// Tile t covers interior points [1 + t*T, min((t+1)*T, n)] (ragged last tile, c10).
-// tile_order = 0: tiles in increasing order; 1: decreasing (used by the
-// order-independence test — the result must not depend on it).
+// §3.3 hierarchical cycle, 1D (Appendix A :548-573), blocks from block_plan.
+// tile_order = 0: blocks in increasing order; 1: decreasing (used by the order-independence
+// test — the result must not depend on it).
 template <typename T>
-void hier_cycle_1d(const Problem1D<T>& p, int64_t tile, int k, int tile_order,
+void hier_cycle_1d(const Problem1D<T>& p, const BlockPlan& bp, int k, int tile_order,
                    const std::vector<T>& xc, std::vector<T>& xn) {
-  const int64_t ntiles = (p.n + tile - 1) / tile;
+  const int64_t nb = (int64_t)bp.start.size();
   std::vector<T> A, B, rhs;
-  for (int64_t tt = 0; tt < ntiles; ++tt) {
-    const int64_t t = tile_order == 0 ? tt : ntiles - 1 - tt;
-    const int64_t lo = 1 + t * tile;                  // first interior point
-    const int64_t hi = std::min((t + 1) * tile, p.n); // last interior point
-    const int64_t w = hi - lo + 1;
+  for (int64_t tt = 0; tt < nb; ++tt) {
+    const int64_t t = tile_order == 0 ? tt : nb - 1 - tt;
+    const int64_t lo = bp.start[t];        // first interior point of the subdomain
+    const int64_t w = bp.width[t];
+    const int64_t hi = lo + w - 1;
     // Step 1: copy the augmented subdomain [lo-1, hi+1] into two containers,
     // and the rhs of the interior points.
     A.assign(xc.begin() + (lo - 1), xc.begin() + (hi + 2));
@@ -128,9 +173,9 @@ void hier_cycle_1d(const Problem1D<T>& p, int64_t tile, int k, int tile_order,
       for (int64_t i = 1; i <= w; ++i) B[i] = update1d<T>(A[i - 1], A[i + 1], rhs[i - 1]);
       std::swap(A, B);
     }
-    // Step 3: write the latest interior values into the NEXT global array
-    // (snapshot semantics c6; latest values c8).
-    for (int64_t i = 1; i <= w; ++i) xn[lo - 1 + i] = A[i];
+    // Step 3: write the latest values of the OWNED points into the NEXT global array
+    // (snapshot semantics c6; latest values c8; ownership PAPER.md:249).
+    for (int64_t g = bp.own_lo[t]; g <= bp.own_hi[t]; ++g) xn[g] = A[g - lo + 1];
   }
 }
 
@@ -181,21 +226,21 @@ void classic_sweep_2d(const Problem2D<T>& p, const std::vector<T>& x0, std::vect
                                     x0[at(p, i, j + 1)], p.h2f[(j - 1) * p.nx + (i - 1)]);
 }
 
-// §4.1 hierarchical cycle, 2D, o = 0.  Tile (a, b) covers
-// interior x in [1 + a*Tx, min((a+1)*Tx, nx)], y in [1 + b*Ty, min((b+1)*Ty, ny)].
-// The augmented subdomain is (w+2) x (hgt+2); the halo is frozen.
+// §4.1 hierarchical cycle, 2D.  Block (a, b) = x-block a of bx times y-block b
+// of by; the augmented subdomain is (w+2) x (hgt+2); the halo is frozen.  A point
+// is written by the block owning it in both x and y (§4.3).
 template <typename T>
-void hier_cycle_2d(const Problem2D<T>& p, int64_t tx, int64_t ty, int k, int tile_order,
-                   const std::vector<T>& xc, std::vector<T>& xn) {
-  const int64_t ntx = (p.nx + tx - 1) / tx, nty = (p.ny + ty - 1) / ty;
+void hier_cycle_2d(const Problem2D<T>& p, const BlockPlan& bx, const BlockPlan& by, int k,
+                   int tile_order, const std::vector<T>& xc, std::vector<T>& xn) {
+  const int64_t ntx = (int64_t)bx.start.size(), nty = (int64_t)by.start.size();
   const int64_t ntiles = ntx * nty;
   std::vector<T> A, B, rhs;
   for (int64_t tt = 0; tt < ntiles; ++tt) {
     const int64_t t = tile_order == 0 ? tt : ntiles - 1 - tt;
     const int64_t a = t % ntx, b = t / ntx;
-    const int64_t ilo = 1 + a * tx, ihi = std::min((a + 1) * tx, p.nx);
-    const int64_t jlo = 1 + b * ty, jhi = std::min((b + 1) * ty, p.ny);
-    const int64_t w = ihi - ilo + 1, hgt = jhi - jlo + 1, lp = w + 2;
+    const int64_t ilo = bx.start[a], w = bx.width[a];
+    const int64_t jlo = by.start[b], hgt = by.width[b];
+    const int64_t lp = w + 2;
     // Step 1: copy the augmented subdomain (two containers) and the local rhs.
     A.assign((size_t)(lp * (hgt + 2)), T(0));
     for (int64_t jj = 0; jj < hgt + 2; ++jj)
@@ -213,9 +258,10 @@ void hier_cycle_2d(const Problem2D<T>& p, int64_t tx, int64_t ty, int k, int til
                                         A[(jj + 1) * lp + ii], rhs[(jj - 1) * w + (ii - 1)]);
       std::swap(A, B);
     }
-    // Step 3: write the interior into the next global array.
-    for (int64_t jj = 1; jj <= hgt; ++jj)
-      for (int64_t ii = 1; ii <= w; ++ii) xn[at(p, ilo - 1 + ii, jlo - 1 + jj)] = A[jj * lp + ii];
+    // Step 3: write the owned points into the next global array.
+    for (int64_t j = by.own_lo[b]; j <= by.own_hi[b]; ++j)
+      for (int64_t i = bx.own_lo[a]; i <= bx.own_hi[a]; ++i)
+        xn[at(p, i, j)] = A[(j - jlo + 1) * lp + (i - ilo + 1)];
   }
 }
 
@@ -263,8 +309,9 @@ DriverOut drive(double h2, double tol, int tol_mode, double ref_residual, int64_
 
 template <typename T>
 int solve1d(int64_t n, double h, const double* f, const double* bc, const double* x0, int mode,
-            int64_t tile, int k, double tol, int tol_mode, double ref_residual, int64_t max_cycles,
-            int tile_order, double* x_out, double* hist, int64_t* cycles, int* converged) {
+            int64_t tile, int64_t overlap, int k, double tol, int tol_mode, double ref_residual,
+            int64_t max_cycles, int tile_order, double* x_out, double* hist, int64_t* cycles,
+            int* converged) {
   Problem1D<T> p;
   p.n = n;
   p.h2 = h * h;
@@ -280,9 +327,10 @@ int solve1d(int64_t n, double h, const double* f, const double* bc, const double
   for (int64_t i = 0; i < n; ++i) xa[i + 1] = x0 ? (T)x0[i] : T(0);
   std::vector<T>* cur = &xa;
   std::vector<T>* nxt = &xb;
+  const BlockPlan bp = mode == 1 ? BlockPlan() : block_plan(n, tile, overlap);
   auto cycle = [&]() {
     if (mode == 1) classic_sweep_1d(p, *cur, *nxt);
-    else hier_cycle_1d(p, tile, k, tile_order, *cur, *nxt);
+    else hier_cycle_1d(p, bp, k, tile_order, *cur, *nxt);
     std::swap(cur, nxt);
   };
   auto resid = [&]() { return residual_sq_1d(p, *cur); };
@@ -295,9 +343,9 @@ int solve1d(int64_t n, double h, const double* f, const double* bc, const double
 
 template <typename T>
 int solve2d(int64_t nx, int64_t ny, double h, const double* f, const double* bc, const double* x0,
-            int mode, int64_t tx, int64_t ty, int k, double tol, int tol_mode, double ref_residual,
-            int64_t max_cycles, int tile_order, double* x_out, double* hist, int64_t* cycles,
-            int* converged) {
+            int mode, int64_t tx, int64_t ty, int64_t ox, int64_t oy, int k, double tol, int tol_mode,
+            double ref_residual, int64_t max_cycles, int tile_order, double* x_out, double* hist,
+            int64_t* cycles, int* converged) {
   Problem2D<T> p;
   p.nx = nx;
   p.ny = ny;
@@ -325,9 +373,11 @@ int solve2d(int64_t nx, int64_t ny, double h, const double* f, const double* bc,
     for (int64_t i = 1; i <= nx; ++i) xa[at(p, i, j)] = x0 ? (T)x0[(j - 1) * nx + (i - 1)] : T(0);
   std::vector<T>* cur = &xa;
   std::vector<T>* nxt = &xb;
+  const BlockPlan bx = mode == 1 ? BlockPlan() : block_plan(nx, tx, ox);
+  const BlockPlan by = mode == 1 ? BlockPlan() : block_plan(ny, ty, oy);
   auto cycle = [&]() {
     if (mode == 1) classic_sweep_2d(p, *cur, *nxt);
-    else hier_cycle_2d(p, tx, ty, k, tile_order, *cur, *nxt);
+    else hier_cycle_2d(p, bx, by, k, tile_order, *cur, *nxt);
     std::swap(cur, nxt);
   };
   auto resid = [&]() { return residual_sq_2d(p, *cur); };
@@ -347,31 +397,53 @@ extern "C" {
 // dim 1: ny must be 1 and tile_y is ignored.  dtype 0 = double, 1 = float.
 // x_out: nx*ny doubles.  hist: max_cycles+1 doubles or NULL.
 // Returns 0 converged, 1 not converged, 2 invalid argument, 4 non-finite residual.
+// overlap_x/overlap_y: the paper's o (even, 0 <= o < tile).
 int hjo_solve(int dim, int64_t nx, int64_t ny, double h, const double* f, const double* bc,
-              const double* x0, int mode, int dtype, int64_t tile_x, int64_t tile_y, int k,
-              double tol, int tol_mode, double ref_residual, int64_t max_cycles, int tile_order,
-              double* x_out, double* hist, int64_t* cycles, int* converged) {
+              const double* x0, int mode, int dtype, int64_t tile_x, int64_t tile_y,
+              int64_t overlap_x, int64_t overlap_y, int k, double tol, int tol_mode,
+              double ref_residual, int64_t max_cycles, int tile_order, double* x_out, double* hist,
+              int64_t* cycles, int* converged) {
   if (!f || !x_out || !cycles || !converged) return ST_INVALID;
   if (!(h > 0.0) || !std::isfinite(h) || nx < 1 || ny < 1 || max_cycles < 0) return ST_INVALID;
   if (mode != 0 && mode != 1) return ST_INVALID;
   if (mode == 0 && (k < 1 || tile_x < 1 || tile_x > nx)) return ST_INVALID;
+  if (mode == 0 && (overlap_x < 0 || overlap_x % 2 != 0 || overlap_x >= tile_x)) return ST_INVALID;
   if (dim == 1) {
     if (ny != 1) return ST_INVALID;
     if (dtype == 0)
-      return solve1d<double>(nx, h, f, bc, x0, mode, tile_x, k, tol, tol_mode, ref_residual,
-                             max_cycles, tile_order, x_out, hist, cycles, converged);
-    return solve1d<float>(nx, h, f, bc, x0, mode, tile_x, k, tol, tol_mode, ref_residual,
+      return solve1d<double>(nx, h, f, bc, x0, mode, tile_x, overlap_x, k, tol, tol_mode,
+                             ref_residual, max_cycles, tile_order, x_out, hist, cycles, converged);
+    return solve1d<float>(nx, h, f, bc, x0, mode, tile_x, overlap_x, k, tol, tol_mode, ref_residual,
                           max_cycles, tile_order, x_out, hist, cycles, converged);
   }
   if (dim == 2) {
     if (mode == 0 && (tile_y < 1 || tile_y > ny)) return ST_INVALID;
+    if (mode == 0 && (overlap_y < 0 || overlap_y % 2 != 0 || overlap_y >= tile_y)) return ST_INVALID;
     if (dtype == 0)
-      return solve2d<double>(nx, ny, h, f, bc, x0, mode, tile_x, tile_y, k, tol, tol_mode,
-                             ref_residual, max_cycles, tile_order, x_out, hist, cycles, converged);
-    return solve2d<float>(nx, ny, h, f, bc, x0, mode, tile_x, tile_y, k, tol, tol_mode,
-                          ref_residual, max_cycles, tile_order, x_out, hist, cycles, converged);
+      return solve2d<double>(nx, ny, h, f, bc, x0, mode, tile_x, tile_y, overlap_x, overlap_y, k,
+                             tol, tol_mode, ref_residual, max_cycles, tile_order, x_out, hist,
+                             cycles, converged);
+    return solve2d<float>(nx, ny, h, f, bc, x0, mode, tile_x, tile_y, overlap_x, overlap_y, k, tol,
+                          tol_mode, ref_residual, max_cycles, tile_order, x_out, hist, cycles,
+                          converged);
   }
   return ST_INVALID;
+}
+
+// The block plan of one dimension (1-based, inclusive ranges); returns the block count, fills
+// at most cap entries of each output array.  -1 on invalid input.
+int64_t hjo_block_plan(int64_t n, int64_t tile, int64_t overlap, int64_t cap, int64_t* start,
+                       int64_t* width, int64_t* own_lo, int64_t* own_hi) {
+  if (n < 1 || tile < 1 || tile > n || overlap < 0 || overlap % 2 != 0 || overlap >= tile) return -1;
+  const BlockPlan P = block_plan(n, tile, overlap);
+  const int64_t nb = (int64_t)P.start.size();
+  for (int64_t b = 0; b < nb && b < cap; ++b) {
+    start[b] = P.start[b];
+    width[b] = P.width[b];
+    own_lo[b] = P.own_lo[b];
+    own_hi[b] = P.own_hi[b];
+  }
+  return nb;
 }
 
 // ||f - A x||_2 for interior x (double), A = (1/h^2) * stencil, ring from bc.
@@ -418,17 +490,21 @@ double hjo_residual(int dim, int64_t nx, int64_t ny, double h, const double* f, 
 //   smem    = 8 * (2*(Tx+2) + Tx)            1D       (PAPER.md:175; 800 B at Tx=32, :215)
 //           = 8 * (2*(Tx+2)*(Ty+2) + Tx*Ty)  2D       (PAPER.md:389; 26,688 B at 32x32, :425)
 // bytes_per_value lets fp32 report 4-byte figures ("4 bytes for floats").
-int hjo_resource_figures(int dim, int64_t nx, int64_t ny, int64_t tx, int64_t ty,
-                         int64_t bytes_per_value, int64_t* tiles, int64_t* threads, int64_t* smem) {
-  if (tx < 1 || tx > nx) return ST_INVALID;
+// With overlap o (PAPER.md:293-305, Eqs. 7-9; :491-508, Eqs. 12-14): operational blocks =
+// (N - o)/(tpb - o) per dimension (ceiling when inexact = the plan's length), threads =
+// blocks * tpb.
+int hjo_resource_figures(int dim, int64_t nx, int64_t ny, int64_t tx, int64_t ty, int64_t ox,
+                         int64_t oy, int64_t bytes_per_value, int64_t* tiles, int64_t* threads,
+                         int64_t* smem) {
+  if (tx < 1 || tx > nx || ox < 0 || ox % 2 != 0 || ox >= tx) return ST_INVALID;
   if (dim == 1) {
-    *tiles = (nx + tx - 1) / tx;
+    *tiles = (int64_t)block_plan(nx, tx, ox).start.size();
     *threads = *tiles * tx;
     *smem = bytes_per_value * (2 * (tx + 2) + tx);
     return ST_OK;
   }
-  if (dim != 2 || ty < 1 || ty > ny) return ST_INVALID;
-  *tiles = ((nx + tx - 1) / tx) * ((ny + ty - 1) / ty);
+  if (dim != 2 || ty < 1 || ty > ny || oy < 0 || oy % 2 != 0 || oy >= ty) return ST_INVALID;
+  *tiles = (int64_t)(block_plan(nx, tx, ox).start.size() * block_plan(ny, ty, oy).start.size());
   *threads = *tiles * tx * ty;
   *smem = bytes_per_value * (2 * (tx + 2) * (ty + 2) + tx * ty);
   return ST_OK;

@@ -30,22 +30,49 @@ def neighbours(dim, i, j):
     return [(i - 1, j), (i + 1, j), (i, j - 1), (i, j + 1)]
 
 
-def tiles(dim, nx, ny, tx, ty):
-    """Interior index ranges of the o=0 tiles, ragged last tile (reading c10)."""
+def plan_1d(n, T, o):
+    """Blocks along one dimension written out by hand from the paper's rule (independent of the
+    oracle's block_plan): o = 0 -> consecutive tiles, ragged last (reading c10); o > 0 -> starts
+    1 + b(T-o), last block shifted to end at n, half-split ownership with the left block taking
+    the odd extra point.  Returns [(lo, hi, own_lo, own_hi)]."""
+    if o == 0:
+        return [(s, min(s + T - 1, n), s, min(s + T - 1, n)) for s in range(1, n + 1, T)]
+    starts = []
+    s = 1
+    while True:
+        if s + T - 1 >= n:
+            starts.append(n - T + 1)
+            break
+        starts.append(s)
+        s += T - o
+    blocks = [[st, st + T - 1, None, None] for st in starts]
+    blocks[0][2], blocks[-1][3] = 1, n
+    for a, b in zip(blocks, blocks[1:]):
+        overlap = list(range(b[0], a[1] + 1))
+        left = (len(overlap) + 1) // 2
+        a[3] = overlap[left - 1]
+        b[2] = overlap[left - 1] + 1
+    return [tuple(x) for x in blocks]
+
+
+def tiles(dim, nx, ny, tx, ty, ox=0, oy=0):
+    """(interior points, owned points) of every block."""
     out = []
+    px = plan_1d(nx, tx, ox)
     if dim == 1:
-        for a in range((nx + tx - 1) // tx):
-            out.append([(i, 0) for i in range(1 + a * tx, min((a + 1) * tx, nx) + 1)])
+        for lo, hi, a0, a1 in px:
+            out.append(([(i, 0) for i in range(lo, hi + 1)], [(i, 0) for i in range(a0, a1 + 1)]))
         return out
-    for b in range((ny + ty - 1) // ty):
-        for a in range((nx + tx - 1) // tx):
-            out.append([(i, j) for j in range(1 + b * ty, min((b + 1) * ty, ny) + 1)
-                        for i in range(1 + a * tx, min((a + 1) * tx, nx) + 1)])
+    py = plan_1d(ny, ty, oy)
+    for ylo, yhi, b0, b1 in py:
+        for xlo, xhi, a0, a1 in px:
+            out.append(([(i, j) for j in range(ylo, yhi + 1) for i in range(xlo, xhi + 1)],
+                        [(i, j) for j in range(b0, b1 + 1) for i in range(a0, a1 + 1)]))
     return out
 
 
-def cycle_affine(dim, nx, ny, h, f, tx, ty, k):
-    """Dense (M, g) with x_next_interior = M @ z_ringed + g  (o = 0)."""
+def cycle_affine(dim, nx, ny, h, f, tx, ty, k, ox=0, oy=0):
+    """Dense (M, g) with x_next_interior = M @ z_ringed + g (rows from the owning block)."""
     if dim == 1:
         ny = 1
     nz = (nx + 2) if dim == 1 else (nx + 2) * (ny + 2)
@@ -57,7 +84,7 @@ def cycle_affine(dim, nx, ny, h, f, tx, ty, k):
     out_pos = {p: q for q, p in enumerate(interior)}
     M = np.zeros((len(interior), nz))
     g = np.zeros(len(interior))
-    for T in tiles(dim, nx, ny, tx, ty):
+    for T, owned in tiles(dim, nx, ny, tx, ty, ox, oy):
         loc = {p: q for q, p in enumerate(T)}
         w = len(T)
         J = np.zeros((w, w))
@@ -80,9 +107,9 @@ def cycle_affine(dim, nx, ny, h, f, tx, ty, k):
             Jp = Jp @ J
         Mt += S @ B
         gt = S @ d
-        for q, p in enumerate(T):
-            M[out_pos[p]] = Mt[q]
-            g[out_pos[p]] = gt[q]
+        for p in owned:
+            M[out_pos[p]] = Mt[loc[p]]
+            g[out_pos[p]] = gt[loc[p]]
     return M, g, interior, idx
 
 
