@@ -43,7 +43,8 @@ typedef enum {
   HJ_OK = 0,
   HJ_NOT_CONVERGED = 1,      /* outputs valid, cycles == max_cycles                           */
   HJ_ERR_INVALID_ARG = 2,    /* NULL pointer, dim not 1/2, n < 1, h <= 0 or non-finite, ...    */
-  HJ_ERR_INVALID_CONFIG = 3, /* tile < 1 or > n, k < 1 (classic: k != 1), overlap != 0,
+  HJ_ERR_INVALID_CONFIG = 3, /* tile < 1 or > n, k < 1 (classic: k != 1), overlap odd / < 0 /
+                                >= tile, overlap with row slabs,
                                 tol < 0 / >= 1 (relative) / NaN, max_cycles < 0, tile does not
                                 fit on chip, slab rows not a multiple of tile_y              */
   HJ_ERR_NUMERIC = 4,        /* NaN/Inf residual                                               */
@@ -76,12 +77,17 @@ typedef struct {
   hj_dtype dtype;
   int32_t tile_x, tile_y;  /* subdomain interior (the paper's blockDim.x/.y); dim 1: tile_y=1 */
   int32_t k;               /* sub-iterations per cycle (>= 1; classic: 1)                    */
-  int32_t overlap;         /* must be 0 in this version (overlapping subdomains: next)       */
+  int32_t overlap;         /* overlapping subdomains o (x; and y unless overlap_y >= 0): even,
+                              0 <= o < tile.  Block b starts at 1 + b*(tile - o), the last block
+                              is shifted to end at n, overlaps are owned half/half with the left
+                              block taking the odd extra point (PAPER.md:243-305 §3.5, :454-510
+                              §4.3; reading c21).  0 = the paper's basic method.     */
   double tol;
   hj_tol_mode tol_mode;
   double ref_residual;     /* 0: r_0 = ||f - A x0||; > 0: use this r_0 (resume a solve)      */
   int64_t max_cycles;      /* >= 0                                                            */
   hj_kernel kernel;        /* kernel family selection (HJ_KERNEL_AUTO recommended)           */
+  int32_t overlap_y;       /* 2D: overlap along y; negative = same as overlap                 */
 } hj_params;
 
 typedef struct {
@@ -146,8 +152,9 @@ hj_status hj_plan_create_dist(const hj_problem *problem, const hj_params *params
 hj_status jacobi_solve_dist(const hj_problem *problem, const hj_params *params,
                             hj_result *result, const hj_dist *dist);
 
-/* Resource figures of the paper (o = 0): tiles = the paper's block count,
- * threads = tiles*tile_x*tile_y, smem_bytes_paper_formula = sizeof(T)*(2(Tx+2)+Tx) in 1D
+/* Resource figures of the paper: tiles = the paper's operational block count (
+ * with overlap Eq. 8/13, ceiling when inexact), threads = tiles*tile_x*tile_y
+ * (Eq. 9/14), smem_bytes_paper_formula = sizeof(T)*(2(Tx+2)+Tx) in 1D
  * and sizeof(T)*(2(Tx+2)(Ty+2)+TxTy) in 2D. Host-only. */
 hj_status hj_resource_figures(const hj_problem *problem, const hj_params *params,
                               int64_t *tiles, int64_t *threads, int64_t *smem_bytes_paper_formula);

@@ -232,7 +232,13 @@ hj_status validate(const hj_problem* pb, const hj_params* pr, bool need_f) {
   if (pb->nx > (1LL << 30) || pb->ny > (1LL << 30)) { set_error("grid too large"); return HJ_ERR_INVALID_ARG; }
   if (pr->mode != HJ_HIERARCHICAL && pr->mode != HJ_CLASSIC) { set_error("bad mode"); return HJ_ERR_INVALID_CONFIG; }
   if (pr->dtype != HJ_F64 && pr->dtype != HJ_F32) { set_error("bad dtype"); return HJ_ERR_INVALID_CONFIG; }
-  if (pr->overlap != 0) { set_error("overlap must be 0 in this version"); return HJ_ERR_INVALID_CONFIG; }
+  if (pr->mode == HJ_HIERARCHICAL) {
+    const int ox = pr->overlap, oy = pb->dim == 2 ? (pr->overlap_y < 0 ? pr->overlap : pr->overlap_y) : 0;
+    if (ox < 0 || (ox & 1) || ox >= pr->tile_x || oy < 0 || (oy & 1) || (pb->dim == 2 && oy >= pr->tile_y)) {
+      set_error("overlap must be even and in [0, tile) (PAPER.md:249)");
+      return HJ_ERR_INVALID_CONFIG;
+    }
+  }
   if (std::isnan(pr->tol) || pr->tol < 0.0 || (pr->tol_mode == HJ_TOL_RELATIVE && pr->tol >= 1.0)) {
     set_error("tol must be in [0, 1) (relative) or >= 0 (absolute)");
     return HJ_ERR_INVALID_CONFIG;
@@ -267,7 +273,8 @@ static hj_status choose_kernel(const hj_problem* pb, const hj_params* pr, int* k
     return HJ_OK;
   }
   const int t = pr->tile_x;
-  if (pr->kernel == HJ_KERNEL_AUTO && t % 32 == 0 && t <= 1024 && ((t / 32) & (t / 32 - 1)) == 0) {
+  if (pr->kernel == HJ_KERNEL_AUTO && pr->overlap == 0 && t % 32 == 0 && t <= 1024 &&
+      ((t / 32) & (t / 32 - 1)) == 0) {
     *kind = K_REG1D;
     return HJ_OK;
   }
@@ -306,12 +313,22 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
   g.col0 = 16 / esz;
   // tiles / partial layout
   const long long gy0 = di ? di->row_begin : 0;
+  g.ox = pr->mode == HJ_HIERARCHICAL ? pr->overlap : 0;
+  g.oy = (pr->mode == HJ_HIERARCHICAL && pb->dim == 2) ? (pr->overlap_y < 0 ? pr->overlap : pr->overlap_y) : 0;
+  if (di && (g.ox || g.oy)) {
+    delete P;
+    set_error("overlapping subdomains are not supported with row slabs");
+    return HJ_ERR_INVALID_CONFIG;
+  }
   switch (g.kernel_kind) {
     case K_REG2D: case K_SMEM2D:
-      g.ntx = (g.nx + g.tx - 1) / g.tx;
-      g.nty = (g.ny + g.ty - 1) / g.ty;
+      g.ax = make_axis((int)g.nx, g.tx, g.ox);
+      g.ay = make_axis((int)g.ny, g.ty, g.oy);
+      g.ntx = g.ax.nb;
+      g.nty = g.ay.nb;
       g.nrg_global = (ny_global + g.ty - 1) / g.ty;
       g.rg_offset = gy0 / g.ty;
+      if (!di) g.nrg_global = g.nty;
       break;
     case K_CLASSIC2D:
       g.ntx = (g.nx + CLASSIC2D_COLS - 1) / CLASSIC2D_COLS;
@@ -320,7 +337,8 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
       g.rg_offset = gy0 / CLASSIC2D_ROWS;
       break;
     case K_REG1D: case K_SMEM1D:
-      g.ntx = (g.nx + g.tx - 1) / g.tx; g.nty = 1; g.nrg_global = 1; g.rg_offset = 0;
+      g.ax = make_axis((int)g.nx, g.tx, g.ox);
+      g.ntx = g.ax.nb; g.nty = 1; g.nrg_global = 1; g.rg_offset = 0;
       break;
     default:
       g.ntx = (g.nx + CLASSIC1D_CELLS - 1) / CLASSIC1D_CELLS; g.nty = 1; g.nrg_global = 1; g.rg_offset = 0;
@@ -662,7 +680,9 @@ hj_status hj_resource_figures(const hj_problem* pb, const hj_params* pr, int64_t
     return HJ_OK;
   }
   const long long tx = pr->tile_x, ty = pb->dim == 2 ? pr->tile_y : 1;
-  const long long ntx = (pb->nx + tx - 1) / tx, nty = pb->dim == 2 ? (pb->ny + ty - 1) / ty : 1;
+  const int oy = pb->dim == 2 ? (pr->overlap_y < 0 ? pr->overlap : pr->overlap_y) : 0;
+  const long long ntx = axis_nb((int)pb->nx, (int)tx, pr->overlap);
+  const long long nty = pb->dim == 2 ? axis_nb((int)pb->ny, (int)ty, oy) : 1;
   *tiles = ntx * nty;
   *threads = *tiles * tx * ty;
   *smem = pb->dim == 1 ? esz * (2 * (tx + 2) + tx) : esz * (2 * (tx + 2) * (ty + 2) + tx * ty);

@@ -43,6 +43,33 @@ struct Ctrl {
   double S0, S_last;    // h^2-scaled squared residuals
 };
 
+// Subdomains along one axis (0-based interior indices; §3.5, §4.3; DESIGN.md c10, c21).
+//  o == 0: tiles [b*T, min((b+1)*T, n)), ragged last tile, each owns its whole interior.
+//  o  > 0: block b starts at b*(T-o), the last block at n-T (shifted to end at n); all blocks
+//          are T wide; an overlap of L points between blocks b, b+1 is owned ceil(L/2) / floor(L/2).
+struct Axis {
+  int n, T, o, nb;
+};
+__host__ __device__ __forceinline__ int axis_nb(int n, int T, int o) {
+  return o == 0 ? (n + T - 1) / T : (n - T + (T - o) - 1) / (T - o) + 1;
+}
+__host__ __device__ __forceinline__ Axis make_axis(int n, int T, int o) { return Axis{n, T, o, axis_nb(n, T, o)}; }
+__host__ __device__ __forceinline__ int axis_start(const Axis& a, int b) {
+  return a.o == 0 ? b * a.T : (b == a.nb - 1 ? a.n - a.T : b * (a.T - a.o));
+}
+__host__ __device__ __forceinline__ int axis_width(const Axis& a, int b) {
+  return a.o == 0 ? (a.n - b * a.T < a.T ? a.n - b * a.T : a.T) : a.T;
+}
+__host__ __device__ __forceinline__ int axis_own_hi(const Axis& a, int b) {  // inclusive
+  if (b == a.nb - 1) return a.n - 1;
+  if (a.o == 0) return (b + 1) * a.T - 1;
+  const int s1 = axis_start(a, b + 1), L = axis_start(a, b) + a.T - s1;
+  return s1 + (L + 1) / 2 - 1;
+}
+__host__ __device__ __forceinline__ int axis_own_lo(const Axis& a, int b) {
+  return b == 0 ? 0 : axis_own_hi(a, b - 1) + 1;
+}
+
 // Geometry of the padded iterate buffers (both dims; 1D uses one row).
 //   X[(j) * pitch + col0 - 1 + i],  i = 0..nx+1 along x (i=0: west/left ring),
 //   j = 0..ny+1 along y (j=0: south ring).  col0 = 2 puts interior column 0 on a
@@ -53,6 +80,8 @@ struct Geom {
   int64_t pitch, col0, rows; // X layout (elements)
   int64_t fpitch, frows;     // H2F layout: H2F[j*fpitch + i]
   int tx, ty, k;
+  int ox, oy;                  // overlap along x / y (0: the paper's basic method)
+  Axis ax, ay;                 // block plans (hierarchical modes)
   int variant;                 // REG2D kernel variant (tuning knob, HJ_REG2D_VARIANT)
   int stagger_ns;              // REG2D one-time per-warp start offset (HJ_STAGGER_NS)
   int64_t ntx, nty, ntiles;  // tiles of this plan (classic: row-blocks x col-blocks)

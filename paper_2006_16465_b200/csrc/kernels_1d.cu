@@ -154,7 +154,7 @@ reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restric
 // =============================================================================
 template <typename T>
 __global__ void smem1d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
-                              const T* __restrict__ h2f, int nx, double* __restrict__ part,
+                              const T* __restrict__ h2f, int nx, Axis ax, double* __restrict__ part,
                               const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
@@ -166,8 +166,9 @@ __global__ void smem1d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
   T* rhs = B + L;
   __shared__ double wsum[32];
   const long long t = blockIdx.x;
-  const long long i0 = t * Tn;
-  const int w = (int)lmin(Tn, nx - i0);
+  const long long i0 = axis_start(ax, (int)t);     // interior origin (§3.3, §3.5)
+  const int w = axis_width(ax, (int)t);
+  const int o0 = axis_own_lo(ax, (int)t) - (int)i0, o1 = axis_own_hi(ax, (int)t) - (int)i0;
   const int a = threadIdx.x;
   for (int q = a; q < L; q += Tn) {
     const long long gi = i0 + q;  // padded index, 0 = left ring
@@ -176,10 +177,11 @@ __global__ void smem1d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
     B[q] = v;
   }
   const bool active = a < w;
+  const bool owned = a >= o0 && a <= o1;   // overlapping blocks write only what they own
   if (active) rhs[a] = h2f[i0 + a];
   __syncthreads();
   double s2 = 0.0;
-  if (active) {
+  if (owned) {
     const double s = res1((double)A[a + 1], (double)A[a], (double)A[a + 2], (double)(T(2) * rhs[a]));
     s2 = s * s;
   }
@@ -199,7 +201,7 @@ __global__ void smem1d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
     __syncthreads();
     T* tmp = cur; cur = nxt; nxt = tmp;
   }
-  if (kk > 0 && active) xout[COL0 + i0 + a] = cur[a + 1];
+  if (kk > 0 && owned) xout[COL0 + i0 + a] = cur[a + 1];
 }
 
 // =============================================================================
@@ -275,8 +277,8 @@ cudaError_t launch_1d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
   } else if (g.kernel_kind == K_SMEM1D) {
     const size_t smem = sizeof(T) * (2 * size_t(g.tx + 2) + size_t(g.tx));
     smem1d_kernel<T><<<(unsigned)g.ntiles, g.tx, smem, st>>>((const T*)a.xin, (T*)a.xout,
-                                                              (const T*)a.h2f, (int)g.nx, a.part,
-                                                              a.ctrl, g.k, a.max_cycles);
+                                                              (const T*)a.h2f, (int)g.nx, g.ax,
+                                                              a.part, a.ctrl, g.k, a.max_cycles);
   } else {
     classic1d_kernel<T><<<(unsigned)g.ntiles, 256, 0, st>>>((const T*)a.xin, (T*)a.xout,
                                                              (const T*)a.h2f, (int)g.nx, a.part,

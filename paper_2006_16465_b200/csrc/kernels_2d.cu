@@ -5,6 +5,8 @@
 // and copies the interior back.  PAPER.md:114-133 (§3.2): the classic sweep.
 // Every kernel also reduces the h^2-scaled residual of the snapshot it reads:
 // s = h2f - (4x - ((W+E)+(S+N))), sum of s^2 per tile -> part[tile].
+#include <type_traits>
+
 #include "hj_internal.cuh"
 
 namespace hj {
@@ -47,16 +49,16 @@ struct R2 {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <typename T, bool RAGGED>
+template <typename T, bool MASK>
 struct Tile2 {
   T x[8][4];      // current iterate
   T q[8][4];      // 0.25 * h^2 f
   const T* hxp;   // per-warp smem: frozen W (lx == 0) / E (lx == 7) halo of my 8 rows
   const T* hyp;   // per-warp smem: frozen S (ly == 0) / N (ly == 3) halo of my 4 columns
-  uint32_t act;   // RAGGED: bit 4*i+c set if cell (i, c) is inside the tile
+  uint32_t own;   // MASK (overlapping blocks): bit 4*i+c set if this block owns cell (i, c)
 
   __device__ __forceinline__ bool on(int i, int c) const {
-    return !RAGGED || ((act >> (4 * i + c)) & 1u);
+    return !MASK || ((own >> (4 * i + c)) & 1u);
   }
 
   // N/S neighbour rows across lane rows: row 0 of the lane below is my row 7's N, row 7 of the
@@ -144,7 +146,7 @@ struct Tile2 {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         saved[c] = x[i][c];
-        x[i][c] = on(i, c) ? nw[c] : x[i][c];
+        x[i][c] = nw[c];
       }
     }
   }
@@ -181,14 +183,15 @@ struct Tile2 {
 };
 
 // One full 32x32 tile: smem slot -> registers, refill, fused residual, k sub-iterations, store.
-template <typename T, typename C, typename Refill, typename Store>
+template <typename T, typename C, bool MASK, typename Refill, typename Store>
 __device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __restrict__ sf,
                                            T* __restrict__ so, T* __restrict__ hb, int lane, int kk,
                                            double* __restrict__ part, long long t, Refill&& refill,
-                                           Store&& store, T* __restrict__ gdst, long long pitch) {
+                                           Store&& store, T* __restrict__ gdst, long long pitch,
+                                           int ox0, int ox1, int oy0, int oy1) {
   using V2 = typename VecOf<T>::v2;
   const int lx = lane & 7, ly = lane >> 3;
-  Tile2<T, false> tl;
+  Tile2<T, MASK> tl;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {  // 128-bit shared loads
     const int r = 8 * ly + i;
@@ -205,7 +208,17 @@ __device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __
   hb[96 + lane] = sx[33 * C::BW + C::COL0 + lane];
   tl.hxp = hb + (lx == 0 ? 0 : 32) + 8 * ly;
   tl.hyp = hb + (ly == 0 ? 64 : 96) + 4 * lx;
-  tl.act = 0xffffffffu;
+  tl.own = 0xffffffffu;
+  if (MASK) {  // owned sub-range [ox0, ox1] x [oy0, oy1] of the block (tile-local, inclusive)
+    tl.own = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int r = 8 * ly + i, q = 4 * lx + c;
+        if (r >= oy0 && r <= oy1 && q >= ox0 && q <= ox1) tl.own |= 1u << (4 * i + c);
+      }
+  }
   __syncwarp();
   refill();  // every value of the slot is now in registers or the halo buffer
   // fused residual of the snapshot: a separate pass for fp32 (residual in double, reading
@@ -248,7 +261,14 @@ __device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __
     }
   }
   if (kk == 0) return;  // residual-only pass (after max_cycles)
-  if constexpr (C::TMA_STORE) {
+  if constexpr (MASK) {
+    // overlapping blocks: only the owned points are written
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (tl.on(i, c)) gdst[(8 * ly + i) * pitch + 4 * lx + c] = tl.x[i][c];
+  } else if constexpr (C::TMA_STORE) {
     // registers -> staging tile -> TMA store into the NEXT iterate (snapshot semantics)
     if (lane == 0) bulk_wait_read_all();  // the previous tile's store has read the staging tile
     __syncwarp();
@@ -275,11 +295,11 @@ __device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __
 // Persistent kernel over the FULL 32x32 tiles (ntx_full x nty_full of them; ragged edge tiles,
 // if any, are done by smem2d_kernel in edge mode).  Warp w handles full tiles w, w+W, ...;
 // partials are indexed by the global tile index ty*ntx + tx.
-template <typename T, typename C>
+template <typename T, typename C, bool MASK>
 __global__ void __launch_bounds__(C::WARPS * 32, 1)
 reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
              const __grid_constant__ CUtensorMap tmO, T* __restrict__ xout, long long pitch,
-             int ntx_full, long long nfull, int ntx, double* __restrict__ part,
+             Axis ax, Axis ay, int ntx_full, long long nfull, int ntx, double* __restrict__ part,
              const Ctrl* __restrict__ ctrl, int k, long long max_cycles, int stagger_ns) {
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
@@ -296,8 +316,8 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
   const long long gw = (long long)blockIdx.x * C::WARPS + warp;
   const long long nw = (long long)gridDim.x * C::WARPS;
   if (gw >= nfull) return;
-  auto issue = [&](long long u) {  // u: full-tile index
-    const int cx = (int)(32 * (u % ntx_full)), cy = (int)(32 * (u / ntx_full));
+  auto issue = [&](long long u) {  // u: full-block index; box origin = block's interior origin
+    const int cx = axis_start(ax, (int)(u % ntx_full)), cy = axis_start(ay, (int)(u / ntx_full));
     mbar_arrive_expect_tx(bar, C::XBYTES + C::FBYTES);
     tma_load_2d(slot, &tmX, cx, cy, bar);              // x box: padded rows 32ty.., cols 32tx..
     tma_load_2d(slot + C::XSLOT, &tmF, cx, cy, bar);   // h2f box
@@ -318,9 +338,10 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
   int it = 0;
   for (long long u = gw; u < nfull; u += nw, ++it) {
     mbar_wait(bar, it & 1);
-    const long long tx = u % ntx_full, ty = u / ntx_full;
-    reg2d_tile<T, C>(
-        sx, sf, so, hb, lane, kk, part, ty * ntx + tx,
+    const int tx = (int)(u % ntx_full), ty = (int)(u / ntx_full);
+    const int x0 = axis_start(ax, tx), y0 = axis_start(ay, ty);
+    reg2d_tile<T, C, MASK>(
+        sx, sf, so, hb, lane, kk, part, (long long)ty * ntx + tx,
         [&] {
           if (lane == 0 && u + nw < nfull) {
             fence_proxy_async();  // generic reads of the slot before the TMA overwrite
@@ -329,11 +350,12 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
         },
         [&] {
           if (lane == 0) {
-            tma_store_2d(&tmO, (int)(C::COL0 + 32 * tx), (int)(32 * ty + 1), so);
+            tma_store_2d(&tmO, C::COL0 + x0, y0 + 1, so);
             bulk_commit();
           }
         },
-        xout + (32 * ty + 1) * pitch + C::COL0 + 32 * tx, pitch);
+        xout + ((long long)y0 + 1) * pitch + C::COL0 + x0, pitch, axis_own_lo(ax, tx) - x0,
+        axis_own_hi(ax, tx) - x0, axis_own_lo(ay, ty) - y0, axis_own_hi(ay, ty) - y0);
   }
   if (C::TMA_STORE && lane == 0) bulk_wait_all();
 }
@@ -349,8 +371,9 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
 template <typename T>
 __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
                               const T* __restrict__ h2f, long long pitch, long long fpitch, int nx,
-                              int ny, int ntx, int nty, int edge, double* __restrict__ part,
+                              int ny, Axis ax, Axis ay, int edge, double* __restrict__ part,
                               const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
+  const int ntx = ax.nb, nty = ay.nb;
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
   constexpr int COL0 = 16 / sizeof(T);
@@ -370,8 +393,11 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
     else { tx = blockIdx.x - ncol; ty = nty - 1; }
   }
   const long long t = ty * ntx + tx;
-  const long long i0 = tx * Tx, j0 = ty * Ty;  // interior origin (0-based)
-  const int w = (int)lmin(Tx, nx - i0), hgt = (int)lmin(Ty, ny - j0);
+  const long long i0 = axis_start(ax, (int)tx), j0 = axis_start(ay, (int)ty);  // interior origin
+  const int w = axis_width(ax, (int)tx), hgt = axis_width(ay, (int)ty);
+  // owned sub-range (tile-local, inclusive): the whole tile unless blocks overlap
+  const int ox0 = axis_own_lo(ax, (int)tx) - (int)i0, ox1 = axis_own_hi(ax, (int)tx) - (int)i0;
+  const int oy0 = axis_own_lo(ay, (int)ty) - (int)j0, oy1 = axis_own_hi(ay, (int)ty) - (int)j0;
   const int tid = threadIdx.y * Tx + threadIdx.x, nth = Tx * Ty;
   // Step 1: augmented subdomain into both containers (App. A :549-556)
   for (int q = tid; q < L * (Ty + 2); q += nth) {
@@ -384,12 +410,13 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
   }
   const int a = threadIdx.x, b = threadIdx.y;
   const bool active = a < w && b < hgt;
+  const bool owned = a >= ox0 && a <= ox1 && b >= oy0 && b <= oy1;
   if (active) rhs[b * Tx + a] = h2f[(j0 + b) * fpitch + i0 + a];
   __syncthreads();
   // fused residual of the snapshot
   double s2 = 0.0;
   const int c = (b + 1) * L + (a + 1);
-  if (active) {
+  if (owned) {
     const double s = res2((double)A[c], (double)A[c - 1], (double)A[c + 1], (double)A[c - L],
                           (double)A[c + L], (double)(T(4) * rhs[b * Tx + a]));
     s2 = s * s;
@@ -412,7 +439,7 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
     T* tmp = cur; cur = nxt; nxt = tmp;
   }
   // Step 3: interior back to global (the next iterate)
-  if (kk > 0 && active) xout[(j0 + b + 1) * pitch + COL0 + i0 + a] = cur[c];
+  if (kk > 0 && owned) xout[(j0 + b + 1) * pitch + COL0 + i0 + a] = cur[c];
 }
 
 // =============================================================================
@@ -506,28 +533,33 @@ template <typename T>
 cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
   const size_t smem_paper = sizeof(T) * (2 * size_t(g.tx + 2) * (g.ty + 2) + size_t(g.tx) * g.ty);
   if (g.kernel_kind == K_REG2D) {
-    const long long ntx_full = g.nx / 32, nty_full = g.ny / 32, nfull = ntx_full * nty_full;
+    // o = 0: the full 32x32 tiles here, ragged edge tiles by smem2d in edge mode;
+    // o > 0: every block is a full 32x32 tile (the last one shifted), owned-point stores.
+    const bool ovl = g.ox || g.oy;
+    const long long ntx_full = ovl ? g.ntx : g.nx / 32, nty_full = ovl ? g.nty : g.ny / 32;
+    const long long nfull = ntx_full * nty_full;
     if (nfull > 0) {
-      auto go = [&](auto cfg) {
+      auto go = [&](auto cfg, auto mask) {
         using C = decltype(cfg);
         long long ctas = (nfull + C::WARPS - 1) / C::WARPS;
         if (ctas > grid_hint) ctas = grid_hint;
-        reg2d_kernel<T, C><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
-            *a.tm_in, *a.tm_f, *a.tm_out, (T*)a.xout, g.pitch, (int)ntx_full, nfull, (int)g.ntx,
-            a.part, a.ctrl, g.k, a.max_cycles, g.stagger_ns);
+        reg2d_kernel<T, C, decltype(mask)::value><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
+            *a.tm_in, *a.tm_f, *a.tm_out, (T*)a.xout, g.pitch, g.ax, g.ay, (int)ntx_full, nfull,
+            (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles, g.stagger_ns);
       };
-      if (g.variant == 2) go(R2<T, (sizeof(T) == 8 ? 8 : 12), true, true>{});
-      else go(R2<T>{});
+      if (ovl) go(R2<T>{}, std::true_type{});
+      else if (g.variant == 2) go(R2<T, (sizeof(T) == 8 ? 8 : 12), true, true>{}, std::false_type{});
+      else go(R2<T>{}, std::false_type{});
     }
     const long long nedge = g.ntiles - nfull;
     if (nedge > 0)
       smem2d_kernel<T><<<(unsigned)nedge, dim3(32, 32), smem_paper, st>>>(
           (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
-          (int)g.ntx, (int)g.nty, 1, a.part, a.ctrl, g.k, a.max_cycles);
+          g.ax, g.ay, 1, a.part, a.ctrl, g.k, a.max_cycles);
   } else if (g.kernel_kind == K_SMEM2D) {
     smem2d_kernel<T><<<(unsigned)g.ntiles, dim3(g.tx, g.ty), smem_paper, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
-        (int)g.ntx, (int)g.nty, 0, a.part, a.ctrl, g.k, a.max_cycles);
+        g.ax, g.ay, 0, a.part, a.ctrl, g.k, a.max_cycles);
   } else {
     classic2d_kernel<T><<<(unsigned)(g.ntx * g.nty), 128, 0, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
@@ -541,7 +573,10 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
 
 template <typename T, typename C>
 cudaError_t cfg2() {
-  return cudaFuncSetAttribute(reg2d_kernel<T, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  cudaError_t e = cudaFuncSetAttribute(reg2d_kernel<T, C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)C::SMEM);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(reg2d_kernel<T, C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
 }
 
 cudaError_t configure_2d() {

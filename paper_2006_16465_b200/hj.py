@@ -37,7 +37,7 @@ class hj_params(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int), ("dtype", ctypes.c_int), ("tile_x", ctypes.c_int32),
                 ("tile_y", ctypes.c_int32), ("k", ctypes.c_int32), ("overlap", ctypes.c_int32),
                 ("tol", ctypes.c_double), ("tol_mode", ctypes.c_int), ("ref_residual", ctypes.c_double),
-                ("max_cycles", ctypes.c_int64), ("kernel", ctypes.c_int)]
+                ("max_cycles", ctypes.c_int64), ("kernel", ctypes.c_int), ("overlap_y", ctypes.c_int32)]
 
 
 class hj_result(ctypes.Structure):
@@ -108,8 +108,9 @@ def make_params(mode="hier", dtype="f64", tile=(32, 32), k=None, overlap=0, tol=
     tx, ty = tile if isinstance(tile, (tuple, list)) else (tile, 1)
     if k is None:
         k = 1 if MODES[mode] == 1 else 16
-    return hj_params(MODES[mode], DTYPES[dtype], tx, ty, k, overlap,
-                     float(tol), TOL_MODES[tol_mode], float(ref_residual), int(max_cycles), KERNELS[kernel])
+    ox, oy = overlap if isinstance(overlap, (tuple, list)) else (overlap, -1)
+    return hj_params(MODES[mode], DTYPES[dtype], tx, ty, k, ox,
+                     float(tol), TOL_MODES[tol_mode], float(ref_residual), int(max_cycles), KERNELS[kernel], oy)
 
 
 def _host(a, n, name):

@@ -49,7 +49,7 @@ def test_sass_targets_sm100a():
     (dict(tile=(64, 32)), hj.HJ_ERR_INVALID_CONFIG),     # tile > n
     (dict(tile=(0, 8)), hj.HJ_ERR_INVALID_CONFIG),
     (dict(k=0), hj.HJ_ERR_INVALID_CONFIG),
-    (dict(overlap=2), hj.HJ_ERR_INVALID_CONFIG),
+    (dict(overlap=3), hj.HJ_ERR_INVALID_CONFIG),
     (dict(tol=1.5), hj.HJ_ERR_INVALID_CONFIG),
     (dict(tol=-1.0), hj.HJ_ERR_INVALID_CONFIG),
     (dict(max_cycles=-1), hj.HJ_ERR_INVALID_CONFIG),
