@@ -263,7 +263,14 @@ static hj_status choose_kernel(const hj_problem* pb, const hj_params* pr, int* k
   const size_t esz = pr->dtype == HJ_F64 ? 8 : 4;
   if (pr->mode == HJ_CLASSIC) { *kind = pb->dim == 2 ? K_CLASSIC2D : K_CLASSIC1D; return HJ_OK; }
   if (pb->dim == 2) {
-    if (pr->kernel == HJ_KERNEL_AUTO && pr->tile_x == 32 && pr->tile_y == 32) { *kind = K_REG2D; return HJ_OK; }
+    // TMA box origins must be 16-byte aligned along x: with overlapping blocks every block start
+    // b*(32-o) and the shifted last start nx-32 must be a multiple of 16/sizeof(T) elements.
+    const long long al = 16 / (long long)esz;
+    const bool aligned = pr->overlap == 0 || ((32 - pr->overlap) % al == 0 && (pb->nx - 32) % al == 0);
+    if (pr->kernel == HJ_KERNEL_AUTO && pr->tile_x == 32 && pr->tile_y == 32 && aligned) {
+      *kind = K_REG2D;
+      return HJ_OK;
+    }
     const size_t smem = esz * (2 * size_t(pr->tile_x + 2) * (pr->tile_y + 2) + size_t(pr->tile_x) * pr->tile_y);
     if ((long long)pr->tile_x * pr->tile_y > 1024 || smem > 200 * 1024) {
       set_error("tile does not fit one CTA (tile_x*tile_y <= 1024 and paper smem <= 200 KiB)");

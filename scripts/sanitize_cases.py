@@ -15,6 +15,8 @@ cases = [
     (1, 5000, 1, dict(mode="classic")),
     (2, 100, 70, dict(mode="hier", tile=(32, 32), k=5, overlap=4)),   # overlapping blocks, reg2d
     (2, 40, 30, dict(mode="hier", tile=(8, 8), k=4, overlap=2)),      # overlapping blocks, smem2d
+    (2, 128, 64, dict(mode="hier", tile=(32, 32), k=4, overlap=8, dtype="f32")),
+    (2, 96, 64, dict(mode="hier", tile=(32, 32), k=4, overlap=2, dtype="f32")),
     (1, 1000, 1, dict(mode="hier", tile=64, k=7, overlap=10)),         # overlapping blocks, smem1d
 ]
 for dim, nx, ny, kw in cases:

@@ -18,6 +18,8 @@ COUNTS = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cross
     (2, 100, 70, (32, 32), 5, 4, "auto"),       # register kernel, shifted last blocks
     (2, 96, 64, (32, 32), 16, 2, "auto"),
     (2, 64, 64, (32, 32), 3, (6, 2), "auto"),
+    (2, 99, 70, (32, 32), 4, 4, "auto"),       # odd nx: misaligned last block -> smem kernel
+    (2, 128, 64, (32, 32), 6, 8, "auto"),      # fp32-aligned overlap -> register kernel
     (2, 100, 70, (32, 32), 5, 4, "smem"),
     (2, 40, 30, (8, 8), 4, 2, "auto"),
     (2, 37, 29, (10, 6), 3, (4, 2), "auto"),
