@@ -13,6 +13,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -20,9 +21,10 @@
 #include "hj_internal.cuh"
 #include "hj_plan.h"
 
-// NCCL is resolved at run time (dlopen) rather than linked: the process may already hold
-// torch's bundled libnccl.so.2, and binding the system copy first would break it.  RTLD_NOLOAD
-// reuses an already-loaded libnccl.so.2; otherwise the default search path is used.
+// NCCL is resolved at run time (dlopen) rather than linked: the process may already hold (or
+// later load) torch's bundled libnccl.so.2, and binding another copy first would break it.
+// Order: $HJ_NCCL_LIB (the Python binding points it at torch's wheel), an already-loaded
+// libnccl.so.2, then the default search path.
 namespace {
 struct NcclApi {
   decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
@@ -41,7 +43,9 @@ const NcclApi& nccl() {
   static NcclApi api;
   static std::once_flag once;
   std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    void* h = nullptr;
+    if (const char* path = std::getenv("HJ_NCCL_LIB")) h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (!h) { api.err = dlerror(); return; }
 #define HJ_SYM(name) api.name = reinterpret_cast<decltype(api.name)>(dlsym(h, "nccl" #name)); if (!api.name) { api.err = "missing nccl" #name; return; }

@@ -67,6 +67,15 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() "
                               "(python -m paper_2006_16465_b200.build)")
+        if "HJ_NCCL_LIB" not in os.environ:
+            # share torch's NCCL (if its wheel is installed) instead of the system copy
+            try:
+                import nvidia.nccl
+                p = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+                if os.path.exists(p):
+                    os.environ["HJ_NCCL_LIB"] = p
+            except ImportError:
+                pass
         L = ctypes.CDLL(LIB_PATH)
         pp, pr, res = ctypes.POINTER(hj_problem), ctypes.POINTER(hj_params), ctypes.POINTER(hj_result)
         for name, args in [("jacobi_solve", [pp, pr, res]),

@@ -260,3 +260,43 @@ def test_full_size_16384_sampled_tiles(proto):
             r0 = oracle.residual(2, n, n, p["h"], p["f"], p["bc"], p["x0"])
             np.testing.assert_allclose(d["history"][0].item(), r0, rtol=1e-12)
         del d, xg
+
+
+def test_dist_path_single_rank_matches_single_gpu():
+    """jacobi_solve_dist with one rank (1-rank NCCL communicator, rowpart_local + allreduce path,
+    NCCL inside the graph-captured cycle) reproduces the single-GPU solve bit for bit."""
+    p = make_problem("R", 2, 96, 64)
+    ref = hj.jacobi_solve(2, 96, 64, p["h"], p["f"], p["bc"], p["x0"], mode="hier", tile=(32, 32), k=6,
+                          tol=1e-7, max_cycles=10**5)
+    nid = hj.hj_nccl_unique_id()
+    d = hj.jacobi_solve_dist(96, 64, p["h"], p["f"], p["bc"], p["x0"], rank=0, nranks=1, nccl_id=nid,
+                             row_begin=0, row_end=64, mode="hier", tile=(32, 32), k=6, tol=1e-7,
+                             max_cycles=10**5)
+    assert d["cycles"] == ref["cycles"]
+    assert np.array_equal(d["x"], ref["x"])
+    np.testing.assert_allclose(d["history"], ref["history"], rtol=1e-14, atol=0)
+    # classic through the same path
+    ref = hj.jacobi_solve(2, 96, 64, p["h"], p["f"], p["bc"], p["x0"], mode="classic", tol=0.0, max_cycles=9)
+    d = hj.jacobi_solve_dist(96, 64, p["h"], p["f"], p["bc"], p["x0"], rank=0, nranks=1,
+                             nccl_id=hj.hj_nccl_unique_id(), row_begin=0, row_end=64, mode="classic",
+                             tol=0.0, max_cycles=9)
+    assert np.array_equal(d["x"], ref["x"])
+
+
+def test_dist_plan_single_rank_bench_path():
+    """hj_plan_create_dist (the bench's N>1 entry point) with one rank."""
+    import torch
+    n = 128
+    p = make_problem("P", 2, n)
+    dev = torch.device("cuda:0")
+    t = {k: torch.from_numpy(p[k]).to(dev) for k in ("f", "bc", "x0")}
+    s = torch.cuda.Stream(dev)
+    plan = hj.DistPlan(n, n, p["h"], t["f"], t["bc"], t["x0"], rank=0, nranks=1,
+                       nccl_id=hj.hj_nccl_unique_id(), row_begin=0, row_end=n, stream=s.cuda_stream,
+                       mode="hier", tile=(32, 32), k=16, tol=1e-6, max_cycles=10**5)
+    ms = plan.run(6, timed=True)
+    assert ms > 0
+    plan.reset()
+    r = plan.solve()
+    assert r["converged"] and r["cycles"] == 2515     # cross_impl_counts.json (2D 128^2, 1e-6)
+    plan.close()
