@@ -14,8 +14,12 @@
  *
  * Conventions shared by every entry point
  *  - Arrays are row-major with x fastest: f[j*nx + i], 0 <= i < nx, 0 <= j < ny.
- *  - bc (Dirichlet ring): dim 1: [g_left, g_right]; dim 2: [south(nx) | north(nx) | west(ny) |
- *    east(ny)], south = the row below j = 0.  NULL means g = 0 (the paper's u = 0).
+ *  - dim 1 with ny > 1: ny INDEPENDENT 1D problems of nx points each (the paper's batch of 1024
+ *    copies), row-major f[b*nx + i]; the stopping test uses the norm of the stacked
+ *    residual.
+ *  - bc (Dirichlet ring): dim 1: [g_left, g_right] per problem (problem b at bc[2b], bc[2b+1]);
+ *    dim 2: [south(nx) | north(nx) | west(ny) | east(ny)], south = the row below j = 0.  NULL
+ *    means g = 0 (the paper's u = 0).
  *  - x0 NULL means a zero initial guess (the paper's protocol passes ones).
  *  - Iterates are kept in hj_params.dtype (f64 or f32); the residual is always accumulated in
  *    f64 from s = h^2 f - (stencil applied to x) (h^2-scaled form, reported unscaled).
@@ -65,7 +69,7 @@ typedef enum {
 
 typedef struct {
   int32_t dim;           /* 1 or 2                                                           */
-  int64_t nx, ny;        /* interior points per direction; dim 1 => ny == 1                  */
+  int64_t nx, ny;        /* interior points per direction; dim 1: ny = number of problems     */
   double h;              /* grid spacing (hx == hy == h)                                      */
   const double *f;       /* nx*ny right-hand side of -Δu = f (the paper's b)                  */
   const double *bc;      /* ring values (layout above) or NULL                               */

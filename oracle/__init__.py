@@ -91,7 +91,7 @@ def solve(dim, nx, ny, h, f, bc=None, x0=None, *, mode="hier", dtype="f64", tile
     lib = _load()
     n = nx * ny
     f = _f64(f, n, "f")
-    nbc = 2 if dim == 1 else 2 * nx + 2 * ny
+    nbc = 2 * ny if dim == 1 else 2 * nx + 2 * ny   # dim 1: ny independent problems
     bc = _f64(bc, nbc, "bc")
     x0 = _f64(x0, n, "x0")
     x = np.zeros(n, dtype=np.float64)
@@ -108,7 +108,7 @@ def solve(dim, nx, ny, h, f, bc=None, x0=None, *, mode="hier", dtype="f64", tile
     if st == 2:
         raise ValueError("oracle: invalid argument")
     c = cyc.value
-    return dict(x=x.reshape((ny, nx)) if dim == 2 else x,
+    return dict(x=x.reshape((ny, nx)) if (dim == 2 or ny > 1) else x,
                 history=None if hist is None else hist[: c + 1].copy(),
                 cycles=c, converged=bool(conv.value), status=st)
 
@@ -119,7 +119,7 @@ def residual(dim, nx, ny, h, f, bc, x):
     n = nx * ny
     f = _f64(f, n, "f")
     x = _f64(x, n, "x")
-    bc = _f64(bc, 2 if dim == 1 else 2 * nx + 2 * ny, "bc")
+    bc = _f64(bc, 2 * ny if dim == 1 else 2 * nx + 2 * ny, "bc")
     return lib.hjo_residual(dim, nx, ny, float(h), _ptr(f), _ptr(bc), _ptr(x))
 
 

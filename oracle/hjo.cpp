@@ -52,7 +52,7 @@
 // (1D: nx+2 values).  Ring corners are never read by the 5-point stencil.
 //
 // Boundary-data layout ("bc"), shared with the ABI only by documentation:
-//   1D: [g_left, g_right]
+//   1D: [g_left, g_right] per problem (batched: problem b at bc[2b], bc[2b+1])
 //   2D: [south(nx) | north(nx) | west(ny) | east(ny)]   (south = row y=0)
 //   NULL means homogeneous (the paper's u = 0).
 
@@ -307,35 +307,51 @@ DriverOut drive(double h2, double tol, int tol_mode, double ref_residual, int64_
   return out;
 }
 
+// B independent 1D problems (the paper's "1024 copies"):
+// problem b has interior f[b*n .. b*n+n), ends bc[2b], bc[2b+1]; one cycle advances every problem;
+// the stopping test uses the L2 norm of the stacked residual (sum over problems in order).
 template <typename T>
-int solve1d(int64_t n, double h, const double* f, const double* bc, const double* x0, int mode,
-            int64_t tile, int64_t overlap, int k, double tol, int tol_mode, double ref_residual,
-            int64_t max_cycles, int tile_order, double* x_out, double* hist, int64_t* cycles,
-            int* converged) {
-  Problem1D<T> p;
-  p.n = n;
-  p.h2 = h * h;
-  p.h2f.resize(n);
-  p.h2f64.resize(n);
-  for (int64_t i = 0; i < n; ++i) {
-    p.h2f[i] = (T)(p.h2 * f[i]);
-    p.h2f64[i] = (double)p.h2f[i];  // reading c16: residual of the rounded system
+int solve1d(int64_t n, int64_t batch, double h, const double* f, const double* bc, const double* x0,
+            int mode, int64_t tile, int64_t overlap, int k, double tol, int tol_mode,
+            double ref_residual, int64_t max_cycles, int tile_order, double* x_out, double* hist,
+            int64_t* cycles, int* converged) {
+  std::vector<Problem1D<T>> ps(batch);
+  std::vector<std::vector<T>> xa(batch), xb(batch);
+  for (int64_t b = 0; b < batch; ++b) {
+    Problem1D<T>& p = ps[b];
+    p.n = n;
+    p.h2 = h * h;
+    p.h2f.resize(n);
+    p.h2f64.resize(n);
+    for (int64_t i = 0; i < n; ++i) {
+      p.h2f[i] = (T)(p.h2 * f[b * n + i]);
+      p.h2f64[i] = (double)p.h2f[i];  // reading c16: residual of the rounded system
+    }
+    xa[b].assign(n + 2, T(0));
+    xa[b][0] = bc ? (T)bc[2 * b] : T(0);
+    xa[b][n + 1] = bc ? (T)bc[2 * b + 1] : T(0);
+    xb[b] = xa[b];
+    for (int64_t i = 0; i < n; ++i) xa[b][i + 1] = x0 ? (T)x0[b * n + i] : T(0);
   }
-  std::vector<T> xa(n + 2), xb(n + 2);
-  xa[0] = xb[0] = bc ? (T)bc[0] : T(0);
-  xa[n + 1] = xb[n + 1] = bc ? (T)bc[1] : T(0);
-  for (int64_t i = 0; i < n; ++i) xa[i + 1] = x0 ? (T)x0[i] : T(0);
-  std::vector<T>* cur = &xa;
-  std::vector<T>* nxt = &xb;
+  bool flip = false;  // false: current iterate in xa
   const BlockPlan bp = mode == 1 ? BlockPlan() : block_plan(n, tile, overlap);
   auto cycle = [&]() {
-    if (mode == 1) classic_sweep_1d(p, *cur, *nxt);
-    else hier_cycle_1d(p, bp, k, tile_order, *cur, *nxt);
-    std::swap(cur, nxt);
+    for (int64_t b = 0; b < batch; ++b) {
+      const std::vector<T>& cur = flip ? xb[b] : xa[b];
+      std::vector<T>& nxt = flip ? xa[b] : xb[b];
+      if (mode == 1) classic_sweep_1d(ps[b], cur, nxt);
+      else hier_cycle_1d(ps[b], bp, k, tile_order, cur, nxt);
+    }
+    flip = !flip;
   };
-  auto resid = [&]() { return residual_sq_1d(p, *cur); };
-  DriverOut o = drive(p.h2, tol, tol_mode, ref_residual, max_cycles, hist, cycle, resid);
-  for (int64_t i = 0; i < n; ++i) x_out[i] = (double)(*cur)[i + 1];
+  auto resid = [&]() {
+    double S = 0.0;
+    for (int64_t b = 0; b < batch; ++b) S += residual_sq_1d(ps[b], flip ? xb[b] : xa[b]);
+    return S;
+  };
+  DriverOut o = drive(h * h, tol, tol_mode, ref_residual, max_cycles, hist, cycle, resid);
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < n; ++i) x_out[b * n + i] = (double)(flip ? xb[b] : xa[b])[i + 1];
   *cycles = o.cycles;
   *converged = o.converged;
   return o.status;
@@ -394,7 +410,8 @@ int solve2d(int64_t nx, int64_t ny, double h, const double* f, const double* bc,
 extern "C" {
 
 // Solve -Δu = f with classic (mode 1) or hierarchical (mode 0) Jacobi.
-// dim 1: ny must be 1 and tile_y is ignored.  dtype 0 = double, 1 = float.
+// dim 1: ny = number of independent problems (1 = a single problem), tile_y ignored;
+// bc = [left_0, right_0, left_1, right_1, ...].  dtype 0 = double, 1 = float.
 // x_out: nx*ny doubles.  hist: max_cycles+1 doubles or NULL.
 // Returns 0 converged, 1 not converged, 2 invalid argument, 4 non-finite residual.
 // overlap_x/overlap_y: the paper's o (even, 0 <= o < tile).
@@ -408,13 +425,12 @@ int hjo_solve(int dim, int64_t nx, int64_t ny, double h, const double* f, const 
   if (mode != 0 && mode != 1) return ST_INVALID;
   if (mode == 0 && (k < 1 || tile_x < 1 || tile_x > nx)) return ST_INVALID;
   if (mode == 0 && (overlap_x < 0 || overlap_x % 2 != 0 || overlap_x >= tile_x)) return ST_INVALID;
-  if (dim == 1) {
-    if (ny != 1) return ST_INVALID;
+  if (dim == 1) {  // ny = number of independent problems (batch)
     if (dtype == 0)
-      return solve1d<double>(nx, h, f, bc, x0, mode, tile_x, overlap_x, k, tol, tol_mode,
+      return solve1d<double>(nx, ny, h, f, bc, x0, mode, tile_x, overlap_x, k, tol, tol_mode,
                              ref_residual, max_cycles, tile_order, x_out, hist, cycles, converged);
-    return solve1d<float>(nx, h, f, bc, x0, mode, tile_x, overlap_x, k, tol, tol_mode, ref_residual,
-                          max_cycles, tile_order, x_out, hist, cycles, converged);
+    return solve1d<float>(nx, ny, h, f, bc, x0, mode, tile_x, overlap_x, k, tol, tol_mode,
+                          ref_residual, max_cycles, tile_order, x_out, hist, cycles, converged);
   }
   if (dim == 2) {
     if (mode == 0 && (tile_y < 1 || tile_y > ny)) return ST_INVALID;
@@ -450,17 +466,21 @@ int64_t hjo_block_plan(int64_t n, int64_t tile, int64_t overlap, int64_t cap, in
 double hjo_residual(int dim, int64_t nx, int64_t ny, double h, const double* f, const double* bc,
                     const double* x) {
   const double h2 = h * h;
-  if (dim == 1) {
-    Problem1D<double> p;
-    p.n = nx;
-    p.h2 = h2;
-    p.h2f64.resize(nx);
-    for (int64_t i = 0; i < nx; ++i) p.h2f64[i] = h2 * f[i];
-    std::vector<double> xx(nx + 2);
-    xx[0] = bc ? bc[0] : 0.0;
-    xx[nx + 1] = bc ? bc[1] : 0.0;
-    for (int64_t i = 0; i < nx; ++i) xx[i + 1] = x[i];
-    return std::sqrt(residual_sq_1d(p, xx)) / h2;
+  if (dim == 1) {  // ny independent problems
+    double S = 0.0;
+    for (int64_t b = 0; b < ny; ++b) {
+      Problem1D<double> p;
+      p.n = nx;
+      p.h2 = h2;
+      p.h2f64.resize(nx);
+      for (int64_t i = 0; i < nx; ++i) p.h2f64[i] = h2 * f[b * nx + i];
+      std::vector<double> xx(nx + 2);
+      xx[0] = bc ? bc[2 * b] : 0.0;
+      xx[nx + 1] = bc ? bc[2 * b + 1] : 0.0;
+      for (int64_t i = 0; i < nx; ++i) xx[i + 1] = x[b * nx + i];
+      S += residual_sq_1d(p, xx);
+    }
+    return std::sqrt(S) / h2;
   }
   Problem2D<double> p;
   p.nx = nx;
@@ -497,8 +517,8 @@ int hjo_resource_figures(int dim, int64_t nx, int64_t ny, int64_t tx, int64_t ty
                          int64_t oy, int64_t bytes_per_value, int64_t* tiles, int64_t* threads,
                          int64_t* smem) {
   if (tx < 1 || tx > nx || ox < 0 || ox % 2 != 0 || ox >= tx) return ST_INVALID;
-  if (dim == 1) {
-    *tiles = (int64_t)block_plan(nx, tx, ox).start.size();
+  if (dim == 1) {  // ny independent problems: blocks for all of them
+    *tiles = (int64_t)block_plan(nx, tx, ox).start.size() * ny;
     *threads = *tiles * tx;
     *smem = bytes_per_value * (2 * (tx + 2) + tx);
     return ST_OK;

@@ -47,10 +47,10 @@ __global__ void init_x_kernel(T* __restrict__ X, long long pitch, long long rows
     const long long r = q / pitch, cc = q % pitch;
     const long long i = cc - (col0 - 1);  // padded x index: 0 = west ring, nx+1 = east ring
     T v = T(0);
-    if (dim == 1) {
-      if (i == 0) v = bc ? (T)bc[0] : T(0);
-      else if (i == nx + 1) v = bc ? (T)bc[1] : T(0);
-      else if (i >= 1 && i <= nx && with_interior && x0) v = (T)x0[i - 1];
+    if (dim == 1) {  // row r = independent problem r (its own Dirichlet ends)
+      if (i == 0) v = bc ? (T)bc[2 * r] : T(0);
+      else if (i == nx + 1) v = bc ? (T)bc[2 * r + 1] : T(0);
+      else if (i >= 1 && i <= nx && with_interior && x0) v = (T)x0[r * nx + i - 1];
     } else if (i >= 0 && i <= nx + 1 && r <= ny_local + 1) {
       const long long gj = gy0 + r;  // global padded row
       const bool iin = i >= 1 && i <= nx;
@@ -90,7 +90,7 @@ __global__ void extract_kernel(const T* __restrict__ X, long long pitch, int dim
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
        q += (long long)gridDim.x * blockDim.x) {
     const long long j = q / nx, i = q % nx;
-    out[q] = (double)X[(dim == 1 ? 0 : (j + 1) * pitch) + col0 + i];
+    out[q] = (double)X[(dim == 1 ? j : j + 1) * pitch + col0 + i];
   }
 }
 
@@ -223,8 +223,8 @@ hj_status ensure_configured(int* nsm) {
 hj_status validate(const hj_problem* pb, const hj_params* pr, bool need_f) {
   if (!pb || !pr) { set_error("NULL problem or params"); return HJ_ERR_INVALID_ARG; }
   if (pb->dim != 1 && pb->dim != 2) { set_error("dim must be 1 or 2"); return HJ_ERR_INVALID_ARG; }
-  if (pb->nx < 1 || pb->ny < 1 || (pb->dim == 1 && pb->ny != 1)) {
-    set_error("nx, ny must be >= 1 (dim 1: ny == 1)");
+  if (pb->nx < 1 || pb->ny < 1) {
+    set_error("nx, ny must be >= 1");
     return HJ_ERR_INVALID_ARG;
   }
   if (!(pb->h > 0.0) || !std::isfinite(pb->h)) { set_error("h must be finite and > 0"); return HJ_ERR_INVALID_ARG; }
@@ -343,12 +343,12 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
       g.nrg_global = (ny_global + CLASSIC2D_ROWS - 1) / CLASSIC2D_ROWS;
       g.rg_offset = gy0 / CLASSIC2D_ROWS;
       break;
-    case K_REG1D: case K_SMEM1D:
+    case K_REG1D: case K_SMEM1D:  // one row (= row group) per independent problem
       g.ax = make_axis((int)g.nx, g.tx, g.ox);
-      g.ntx = g.ax.nb; g.nty = 1; g.nrg_global = 1; g.rg_offset = 0;
+      g.ntx = g.ax.nb; g.nty = g.ny; g.nrg_global = g.ny; g.rg_offset = 0;
       break;
     default:
-      g.ntx = (g.nx + CLASSIC1D_CELLS - 1) / CLASSIC1D_CELLS; g.nty = 1; g.nrg_global = 1; g.rg_offset = 0;
+      g.ntx = (g.nx + CLASSIC1D_CELLS - 1) / CLASSIC1D_CELLS; g.nty = g.ny; g.nrg_global = g.ny; g.rg_offset = 0;
   }
   g.ntiles = g.ntx * g.nty;
   g.parts_per_row = g.kernel_kind == K_CLASSIC2D ? 4 * g.ntx : g.ntx;
@@ -363,9 +363,9 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
   } else {
     const long long span = g.ntx * (long long)(g.kernel_kind == K_CLASSIC1D ? CLASSIC1D_CELLS : g.tx);
     g.pitch = round_up(span + 4 * g.col0 + 64, 256 / esz);
-    g.rows = 1;
+    g.rows = g.ny;   // independent problems
     g.fpitch = round_up(span + 64, 128 / esz);
-    g.frows = 1;
+    g.frows = g.ny;
   }
   if (st == nullptr) {
     // The legacy default stream cannot be captured into graphs: run the plan on its own
@@ -414,7 +414,7 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
   PCK(cudaEventCreate(&P->ev1));
   // keep device copies of x0 / bc so that hj_plan_reset can re-initialise
   const long long nloc = g.nx * g.ny;
-  const long long nbc = g.dim == 1 ? 2 : 2 * g.nx + 2 * ny_global;
+  const long long nbc = g.dim == 1 ? 2 * g.ny : 2 * g.nx + 2 * ny_global;
   PCK(cudaMalloc(&P->bc_d, sizeof(double) * nbc));
   if (pb->bc) PCK(cudaMemcpyAsync(P->bc_d, pb->bc, sizeof(double) * nbc, cudaMemcpyDefault, st));
   else PCK(cudaMemsetAsync(P->bc_d, 0, sizeof(double) * nbc, st));
@@ -689,7 +689,7 @@ hj_status hj_resource_figures(const hj_problem* pb, const hj_params* pr, int64_t
   const long long tx = pr->tile_x, ty = pb->dim == 2 ? pr->tile_y : 1;
   const int oy = pb->dim == 2 ? (pr->overlap_y < 0 ? pr->overlap : pr->overlap_y) : 0;
   const long long ntx = axis_nb((int)pb->nx, (int)tx, pr->overlap);
-  const long long nty = pb->dim == 2 ? axis_nb((int)pb->ny, (int)ty, oy) : 1;
+  const long long nty = pb->dim == 2 ? axis_nb((int)pb->ny, (int)ty, oy) : pb->ny;  // 1D: per problem
   *tiles = ntx * nty;
   *threads = *tiles * tx * ty;
   *smem = pb->dim == 1 ? esz * (2 * (tx + 2) + tx) : esz * (2 * (tx + 2) * (ty + 2) + tx * ty);
@@ -745,7 +745,7 @@ hj_status jacobi_solve(const hj_problem* pb, const hj_params* pr, hj_result* res
   }
   auto t0 = std::chrono::steady_clock::now();
   const long long n = pb->nx * pb->ny;
-  const long long nbc = pb->dim == 1 ? 2 : 2 * pb->nx + 2 * pb->ny;
+  const long long nbc = pb->dim == 1 ? 2 * pb->ny : 2 * pb->nx + 2 * pb->ny;
   double *f = nullptr, *bc = nullptr, *x0 = nullptr, *x = nullptr, *hist = nullptr;
   cudaStream_t st;
   HJ_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));

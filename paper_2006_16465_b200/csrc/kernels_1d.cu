@@ -32,10 +32,10 @@ struct R1 {
 
 template <typename T, int C, bool RAGGED>
 __device__ __forceinline__ void reg1d_tile(const T* __restrict__ sx, const T* __restrict__ sf,
-                                           T* __restrict__ xout, long long t, int w, int lane,
-                                           int kk, double* __restrict__ part, uint64_t* bar,
-                                           const T* __restrict__ xin, const T* __restrict__ h2f,
-                                           long long t_next, void* slot_x, void* slot_f) {
+                                           T* __restrict__ xrow, long long t, int w, int lane,
+                                           int kk, double* __restrict__ part, long long u,
+                                           uint64_t* bar, const T* nx_src, const T* nq_src,
+                                           void* slot_x, void* slot_f) {
   using P = R1<T, C>;
   T x[C], q[C];
 #pragma unroll
@@ -69,12 +69,13 @@ __device__ __forceinline__ void reg1d_tile(const T* __restrict__ sx, const T* __
     }
   }
   acc = warp_sum(acc);
-  if (lane == 0) part[t] = acc;
+  if (lane == 0) part[u] = acc;
   __syncwarp();
-  if (lane == 0 && t_next >= 0) {
+  if (lane == 0 && nx_src) {  // the slot is free: prefetch this warp's next tile into it
+    fence_proxy_async();
     mbar_arrive_expect_tx(bar, P::XBYTES + P::FBYTES);
-    bulk_load(slot_x, xin + t_next * P::TILE, P::XBYTES, bar);
-    bulk_load(slot_f, h2f + t_next * P::TILE, P::FBYTES, bar);
+    bulk_load(slot_x, nx_src, P::XBYTES, bar);
+    bulk_load(slot_f, nq_src, P::FBYTES, bar);
   }
 #pragma unroll 1
   for (int s = 0; s < kk; ++s) {
@@ -94,14 +95,16 @@ __device__ __forceinline__ void reg1d_tile(const T* __restrict__ sx, const T* __
   if (kk == 0) return;
 #pragma unroll
   for (int c = 0; c < C; ++c)
-    if (!RAGGED || ((act >> c) & 1u)) xout[P::COL0 + t * P::TILE + C * lane + c] = x[c];
+    if (!RAGGED || ((act >> c) & 1u)) xrow[P::COL0 + t * P::TILE + C * lane + c] = x[c];
 }
 
+// Rows of the padded arrays are independent problems (batched 1D); tile u of the
+// launch is tile (u % ntpr) of problem (u / ntpr), and its residual partial is part[u].
 template <typename T, int C>
 __global__ void __launch_bounds__(R1<T, C>::WARPS * 32)
 reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restrict__ h2f, int nx,
-             long long ntiles, double* __restrict__ part, const Ctrl* __restrict__ ctrl, int k,
-             long long max_cycles) {
+             long long pitch, long long fpitch, int ntpr, long long ntiles,
+             double* __restrict__ part, const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
   using P = R1<T, C>;
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
@@ -115,34 +118,40 @@ reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restric
   const long long gw = (long long)blockIdx.x * P::WARPS + warp;
   const long long nw = (long long)gridDim.x * P::WARPS;
   if (gw >= ntiles) return;
+  auto src_x = [&](long long u) { return xin + (u / ntpr) * pitch + (u % ntpr) * P::TILE; };
+  auto src_q = [&](long long u) { return h2f + (u / ntpr) * fpitch + (u % ntpr) * P::TILE; };
   if (lane == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     fence_mbar_init();
     for (int s = 0; s < 2; ++s) {
-      const long long t = gw + s * nw;
-      if (t < ntiles) {
+      const long long u = gw + s * nw;
+      if (u < ntiles) {
         unsigned char* sl = s ? slot1 : slot0;
         mbar_arrive_expect_tx(&bars[s], P::XBYTES + P::FBYTES);
-        bulk_load(sl, xin + t * P::TILE, P::XBYTES, &bars[s]);
-        bulk_load(sl + P::XSLOT, h2f + t * P::TILE, P::FBYTES, &bars[s]);
+        bulk_load(sl, src_x(u), P::XBYTES, &bars[s]);
+        bulk_load(sl + P::XSLOT, src_q(u), P::FBYTES, &bars[s]);
       }
     }
   }
   __syncwarp();
   int it = 0;
-  for (long long t = gw; t < ntiles; t += nw, ++it) {
+  for (long long u = gw; u < ntiles; u += nw, ++it) {
     const int s = it & 1;
     unsigned char* sl = s ? slot1 : slot0;
     mbar_wait(&bars[s], (it >> 1) & 1);
+    const long long t = u % ntpr;
     const int w = (int)lmin(P::TILE, nx - t * P::TILE);
-    const long long tn = t + 2 * nw < ntiles ? t + 2 * nw : -1;
+    const long long un = u + 2 * nw;
+    const T* nxs = un < ntiles ? src_x(un) : nullptr;
+    const T* nqs = un < ntiles ? src_q(un) : nullptr;
     const T* sx = reinterpret_cast<const T*>(sl);
     const T* sf = reinterpret_cast<const T*>(sl + P::XSLOT);
+    T* xrow = xout + (u / ntpr) * pitch;
     if (w == P::TILE)
-      reg1d_tile<T, C, false>(sx, sf, xout, t, w, lane, kk, part, &bars[s], xin, h2f, tn, sl, sl + P::XSLOT);
+      reg1d_tile<T, C, false>(sx, sf, xrow, t, w, lane, kk, part, u, &bars[s], nxs, nqs, sl, sl + P::XSLOT);
     else
-      reg1d_tile<T, C, true>(sx, sf, xout, t, w, lane, kk, part, &bars[s], xin, h2f, tn, sl, sl + P::XSLOT);
+      reg1d_tile<T, C, true>(sx, sf, xrow, t, w, lane, kk, part, u, &bars[s], nxs, nqs, sl, sl + P::XSLOT);
   }
 }
 
@@ -153,9 +162,15 @@ reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restric
 // buffer (reading c6), rhs of the updated point (reading c7).
 // =============================================================================
 template <typename T>
-__global__ void smem1d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
-                              const T* __restrict__ h2f, int nx, Axis ax, double* __restrict__ part,
+__global__ void smem1d_kernel(const T* __restrict__ xin_all, T* __restrict__ xout_all,
+                              const T* __restrict__ h2f_all, int nx, long long pitch,
+                              long long fpitch, Axis ax, double* __restrict__ part,
                               const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
+  // block = (problem row, subdomain): rows of the padded arrays are independent problems
+  const long long row = blockIdx.x / ax.nb;
+  const T* __restrict__ xin = xin_all + row * pitch;
+  T* __restrict__ xout = xout_all + row * pitch;
+  const T* __restrict__ h2f = h2f_all + row * fpitch;
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
   constexpr int COL0 = 16 / sizeof(T);
@@ -165,7 +180,7 @@ __global__ void smem1d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
   T* B = A + L;
   T* rhs = B + L;
   __shared__ double wsum[32];
-  const long long t = blockIdx.x;
+  const long long t = blockIdx.x % ax.nb;
   const long long i0 = axis_start(ax, (int)t);     // interior origin (§3.3, §3.5)
   const int w = axis_width(ax, (int)t);
   const int o0 = axis_own_lo(ax, (int)t) - (int)i0, o1 = axis_own_hi(ax, (int)t) - (int)i0;
@@ -191,7 +206,7 @@ __global__ void smem1d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
   if (a == 0) {
     double acc = 0.0;
     for (int q = 0; q < (Tn + 31) / 32; ++q) acc += wsum[q];
-    part[t] = acc;
+    part[blockIdx.x] = acc;
   }
   const T q2 = active ? rhs[a] : T(0);
   T* cur = A;
@@ -210,15 +225,20 @@ __global__ void smem1d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
 // =============================================================================
 template <typename T>
 __global__ void __launch_bounds__(256)
-classic1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restrict__ h2f, int nx,
+classic1d_kernel(const T* __restrict__ xin_all, T* __restrict__ xout_all,
+                 const T* __restrict__ h2f_all, int nx, long long pitch, long long fpitch, int ncb,
                  double* __restrict__ part, const Ctrl* __restrict__ ctrl, long long max_cycles) {
+  const long long row = blockIdx.x / ncb;  // independent problem
+  const T* __restrict__ xin = xin_all + row * pitch;
+  T* __restrict__ xout = xout_all + row * pitch;
+  const T* __restrict__ h2f = h2f_all + row * fpitch;
   if (ctrl->done) return;
   const bool write = ctrl->c < max_cycles;
   constexpr int COL0 = 16 / sizeof(T);
   constexpr int V = 8;
   __shared__ double wsum[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long i0 = (long long)blockIdx.x * CLASSIC1D_CELLS + (long long)threadIdx.x * V;
+  const long long i0 = (long long)(blockIdx.x % ncb) * CLASSIC1D_CELLS + (long long)threadIdx.x * V;
   T x[V], f[V];
 #pragma unroll
   for (int c = 0; c < V; ++c) {
@@ -258,8 +278,8 @@ void launch_reg1d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t
   long long ctas = (g.ntiles + P::WARPS - 1) / P::WARPS;
   if (ctas > grid_hint) ctas = grid_hint;
   reg1d_kernel<T, C><<<(unsigned)ctas, P::WARPS * 32, P::SMEM, st>>>(
-      (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (int)g.nx, g.ntiles, a.part, a.ctrl, g.k,
-      a.max_cycles);
+      (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (int)g.nx, g.pitch, g.fpitch, (int)g.ntx,
+      g.ntiles, a.part, a.ctrl, g.k, a.max_cycles);
 }
 
 template <typename T>
@@ -276,13 +296,13 @@ cudaError_t launch_1d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
     }
   } else if (g.kernel_kind == K_SMEM1D) {
     const size_t smem = sizeof(T) * (2 * size_t(g.tx + 2) + size_t(g.tx));
-    smem1d_kernel<T><<<(unsigned)g.ntiles, g.tx, smem, st>>>((const T*)a.xin, (T*)a.xout,
-                                                              (const T*)a.h2f, (int)g.nx, g.ax,
-                                                              a.part, a.ctrl, g.k, a.max_cycles);
+    smem1d_kernel<T><<<(unsigned)g.ntiles, g.tx, smem, st>>>(
+        (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (int)g.nx, g.pitch, g.fpitch, g.ax, a.part,
+        a.ctrl, g.k, a.max_cycles);
   } else {
-    classic1d_kernel<T><<<(unsigned)g.ntiles, 256, 0, st>>>((const T*)a.xin, (T*)a.xout,
-                                                             (const T*)a.h2f, (int)g.nx, a.part,
-                                                             a.ctrl, a.max_cycles);
+    classic1d_kernel<T><<<(unsigned)g.ntiles, 256, 0, st>>>(
+        (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (int)g.nx, g.pitch, g.fpitch, (int)g.ntx, a.part,
+        a.ctrl, a.max_cycles);
   }
   return cudaGetLastError();
 }

@@ -139,7 +139,7 @@ def jacobi_solve(dim, nx, ny, h, f, bc=None, x0=None, *, history=True, **params)
     """Host-buffer solve (H2D/D2H inside).  Returns dict(x, history, cycles, converged, status, ...)."""
     n = nx * ny
     f = _host(f, n, "f")
-    bc = _host(bc, 2 if dim == 1 else 2 * nx + 2 * ny, "bc")
+    bc = _host(bc, 2 * ny if dim == 1 else 2 * nx + 2 * ny, "bc")   # dim 1: per problem
     x0 = _host(x0, n, "x0")
     prm = make_params(**params)
     x = np.empty(n)
@@ -148,7 +148,7 @@ def jacobi_solve(dim, nx, ny, h, f, bc=None, x0=None, *, history=True, **params)
     res = hj_result(x.ctypes.data, _hp(hist), 0, 0, 0.0, 0.0, 0.0, 0.0)
     st = _check(lib().jacobi_solve(ctypes.byref(pb), ctypes.byref(prm), ctypes.byref(res)),
                 ok=(HJ_OK, HJ_NOT_CONVERGED, HJ_ERR_NUMERIC))
-    return _result(res, st, x.reshape((ny, nx)) if dim == 2 else x,
+    return _result(res, st, x.reshape((ny, nx)) if (dim == 2 or ny > 1) else x,
                    None if hist is None else hist[: res.cycles + 1])
 
 
@@ -174,7 +174,7 @@ def jacobi_solve_device(dim, nx, ny, h, f, bc=None, x0=None, *, history=True, st
     s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
     st = _check(lib().jacobi_solve_device(ctypes.byref(pb), ctypes.byref(prm), ctypes.byref(res), s),
                 ok=(HJ_OK, HJ_NOT_CONVERGED, HJ_ERR_NUMERIC))
-    return _result(res, st, x.view(ny, nx) if dim == 2 else x,
+    return _result(res, st, x.view(ny, nx) if (dim == 2 or ny > 1) else x,
                    None if hist is None else hist[: res.cycles + 1])
 
 

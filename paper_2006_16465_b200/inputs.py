@@ -42,9 +42,24 @@ def uniform_pm1(start: int, count: int) -> np.ndarray:
     return 2.0 * u - 1.0
 
 
-def make_problem(protocol: str, dim: int, nx: int, ny: int | None = None, seed: int = SEED):
-    """Return dict(dim, nx, ny, h, f, bc, x0) as float64 numpy arrays."""
+def make_problem(protocol: str, dim: int, nx: int, ny: int | None = None, seed: int = SEED,
+                 batch: int = 1):
+    """Return dict(dim, nx, ny, h, f, bc, x0) as float64 numpy arrays.
+
+    dim 1 with batch > 1: `batch` independent problems stacked row-major (ny = batch); P, M and Q
+    give identical copies (the paper's "1024 copies"), R independent random data.
+    """
     if dim == 1:
+        if batch > 1:
+            one = make_problem(protocol, 1, nx, seed=seed)
+            if protocol == "R":
+                n = nx * batch
+                f = uniform_pm1(seed, n)
+                x0 = uniform_pm1(seed + 7 * n + 13, n)
+                bc = uniform_pm1(seed + n, 2 * batch)
+            else:
+                f, x0, bc = np.tile(one["f"], batch), np.tile(one["x0"], batch), np.tile(one["bc"], batch)
+            return dict(dim=1, nx=nx, ny=batch, h=one["h"], f=f, bc=bc, x0=x0)
         ny = 1
     elif ny is None:
         ny = nx

@@ -14,7 +14,7 @@ dev = torch.device("cuda:0")
 
 
 def solve(dim, n, tol, **kw):
-    p = make_problem(kw.pop("protocol", "P"), dim, n)
+    p = make_problem(kw.pop("protocol", "P"), dim, n, batch=kw.pop("batch", 1))
     t = {k: torch.from_numpy(p[k]).to(dev) for k in ("f", "bc", "x0")}
     torch.cuda.synchronize()
     r = hj.jacobi_solve_device(dim, p["nx"], p["ny"], p["h"], t["f"], t["bc"], t["x0"], tol=tol,
@@ -52,15 +52,15 @@ def table_2d(n=1024, tol=1e-4, ks=(4, 8, 16, 32, 64, 128), overlaps=(0, 2, 4, 6,
     return "\n".join(out)
 
 
-def table_1d(n=1024, tol=1e-4, ks=(4, 8, 16, 32, 64, 128), overlaps=(0, 2, 4, 8, 10, 12)):
+def table_1d(n=1024, tol=1e-4, ks=(4, 8, 16, 32, 64, 128), overlaps=(0, 2, 4, 8, 10, 12), batch=1024):
     out = []
-    c = solve(1, n, tol, mode="classic")
-    out.append(f"### 1D N={n} (single problem), tol {tol} (paper Tables 1 and 3 analogue; the paper batches 1024 copies)\n")
+    c = solve(1, n, tol, mode="classic", batch=batch)
+    out.append(f"### 1D {batch} copies of N={n}, tol {tol} (paper Tables 1 and 3 analogue, PAPER.md:213)\n")
     out.append(f"classic: {c['cycles']} sweeps, {c['seconds_solve']*1e3:.1f} ms\n")
     out.append("| k | o | cycles | ms | speedup vs classic |\n|---|---|---|---|---|")
     for k in ks:
         for o in overlaps:
-            r = solve(1, n, tol, mode="hier", tile=32, k=k, overlap=o)
+            r = solve(1, n, tol, mode="hier", tile=32, k=k, overlap=o, batch=batch)
             out.append(f"| {k} | {o} | {r['cycles']} | {r['seconds_solve']*1e3:.1f} | "
                        f"{c['seconds_solve']/r['seconds_solve']:.2f} |")
     return "\n".join(out)
@@ -88,10 +88,14 @@ def configs():
 
 if __name__ == "__main__":
     parts = ["# Paper experiments on one B200 (fp64, protocol P)\n"]
-    for fn in (configs, table_2d, table_1d):
+    fns = [configs, table_2d, table_1d]
+    if len(sys.argv) > 1:
+        fns = [f for f in fns if f.__name__ in sys.argv[1:]]
+    for fn in fns:
         t0 = time.time()
         parts.append(fn())
         parts.append(f"\n_({fn.__name__}: {time.time()-t0:.0f} s)_\n")
         print(parts[-2], flush=True)
     os.makedirs("gpurun_out", exist_ok=True)
-    open("gpurun_out/paper_tables.md", "w").write("\n".join(parts) + "\n")
+    tag = "_".join(sys.argv[1:]) or "all"
+    open(f"gpurun_out/paper_tables_{tag}.md", "w").write("\n".join(parts) + "\n")

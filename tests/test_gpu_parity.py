@@ -300,3 +300,33 @@ def test_dist_plan_single_rank_bench_path():
     r = plan.solve()
     assert r["converged"] and r["cycles"] == 2515     # cross_impl_counts.json (2D 128^2, 1e-6)
     plan.close()
+
+
+# --------------------------------------------------- batched 1D (NEXT #2) ----------
+@pytest.mark.parametrize("n,B,tile,k,ov,mode,kernel", [
+    (1024, 7, 32, 16, 0, "hier", "auto"),      # register kernel, C = 1
+    (5000, 3, 1024, 5, 0, "hier", "auto"),     # register kernel, ragged last tile
+    (1000, 4, 96, 5, 0, "hier", "auto"),       # shared-memory kernel
+    (1024, 5, 32, 16, 4, "hier", "auto"),      # overlapping subdomains
+    (3000, 6, 1, 1, 0, "classic", "auto"),
+])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_batched_1d_bitwise(n, B, tile, k, ov, mode, kernel, dtype):
+    p = make_problem("R", 1, n, batch=B)
+    kw = dict(mode=mode, tol=0.0, max_cycles=9, dtype=dtype)
+    if mode == "hier":
+        kw.update(tile=tile, k=k, overlap=ov)
+    o = oracle.solve(1, n, B, p["h"], p["f"], p["bc"], p["x0"], **kw)
+    g = hj.jacobi_solve(1, n, B, p["h"], p["f"], p["bc"], p["x0"], kernel=kernel, **kw)
+    assert_parity(o, g)
+
+
+@pytest.mark.parametrize("k,o,cycles", [(1, 0, 128760), (8, 0, 25481), (16, 0, 19555), (16, 4, 8093)])
+def test_paper_1d_workload_counts(k, o, cycles):
+    """The paper's 1D workload: 1024 copies of N = 1024, tpb 32, 1e-4: the counts of
+    the independent implementation (tests/golden/cross_impl_counts*.json)."""
+    p = make_problem("P", 1, 1024, batch=1024)
+    kw = dict(mode="hier", tile=32, k=k, overlap=o) if k > 1 else dict(mode="classic")
+    g = hj.jacobi_solve(1, 1024, 1024, p["h"], p["f"], p["bc"], p["x0"], tol=1e-4, max_cycles=10**6,
+                        history=False, **kw)
+    assert g["converged"] and g["cycles"] == cycles

@@ -313,3 +313,25 @@ def test_driver_edge_cases():
     q["x0"] = xs
     r = run(q, mode="hier", tile=4, k=2, tol=1e-6, max_cycles=10, ref_residual=1.0)
     assert r["cycles"] == 0 and r["converged"]
+
+
+# ---------------------------------------------------------- batched 1D (NEXT #2) --
+def test_batched_1d_rows_are_independent_problems():
+    """ny independent 1D problems: every row equals the single-problem oracle run on
+    that row's data; identical copies converge in the single problem's cycle count."""
+    B, n = 5, 45
+    p = make_problem("R", 1, n, batch=B)
+    r = oracle.solve(1, n, B, p["h"], p["f"], p["bc"], p["x0"], mode="hier", tile=8, k=5, tol=0.0, max_cycles=7)
+    for b in range(B):
+        one = oracle.solve(1, n, 1, p["h"], p["f"][b * n:(b + 1) * n], p["bc"][2 * b:2 * b + 2],
+                           p["x0"][b * n:(b + 1) * n], mode="hier", tile=8, k=5, tol=0.0, max_cycles=7)
+        assert np.array_equal(r["x"][b], one["x"])
+    q = make_problem("P", 1, 1024, batch=4)
+    single = make_problem("P", 1, 1024)
+    for mode, k in (("hier", 16), ("classic", 1)):
+        a = oracle.solve(1, 1024, 4, q["h"], q["f"], q["bc"], q["x0"], mode=mode, tile=32, k=k, tol=1e-4,
+                         max_cycles=10**6, history=False)
+        s = oracle.solve(1, 1024, 1, single["h"], single["f"], single["bc"], single["x0"], mode=mode, tile=32,
+                         k=k, tol=1e-4, max_cycles=10**6, history=False)
+        assert a["cycles"] == s["cycles"]
+    assert oracle.resource_figures(1, 1024, 1024, 32)[0] == 1024 * 32   # PAPER.md:215 block count
