@@ -230,6 +230,14 @@ def main():
     else:
         plan.close()
 
+    # the classic global-memory sweep on the same grid (comparison for the time-to-tol projection)
+    classic_ms = None
+    if world == 1 and args.mode == "hier":
+        cplan = hj.Plan(2, n, n, h, f, bc, x0, stream=stream, mode="classic", tol=0.0, max_cycles=1 << 62)
+        cplan.run(4, timed=True)
+        classic_ms = cplan.run(20, timed=True) / 20
+        cplan.close()
+
     # end to end through the public C-ABI with host buffers (pinned), H2D/D2H inside
     e2e = None
     if world == 1:
@@ -261,9 +269,18 @@ def main():
                "sample": f"1 cycle of the same method on a {side}^2 grid (1/4 of the workload's cells; "
                          f"identical per-cell work), {dt:.1f} s single-threaded"}
     proj = None
-    if ttt is not None:
-        proj = {"tol": 1e-6, "cycles_model": 6.1e6, "seconds": 6.1e6 * ms_step * 1e-3, "measured": False,
-                "note": "projected: steady per-cycle time x model cycle count (SURVEY.md §8(d))"}
+    conv = os.path.join(ROOT, "profiles", "r01_convergence_scaling.json")
+    if world == 1 and args.mode == "hier" and k == K_SUB and n == N_GRID and os.path.exists(conv):
+        fit = json.load(open(conv))["fit"]
+        cyc = fit["hier_k16_o0"]["cycles_16384"]
+        proj = {"tol": 1e-6, "measured": False, "cycles_projected": cyc, "seconds": cyc * ms_step * 1e-3,
+                "basis": "power-law fit of measured cycles-to-1e-6 at 1024^2..4096^2 (profiles/"
+                         "r01_convergence_scaling.json) x the measured cycle time"}
+        if classic_ms:
+            ccyc = fit["classic"]["cycles_16384"]
+            proj["classic_sweeps_projected"] = ccyc
+            proj["classic_seconds"] = ccyc * classic_ms * 1e-3
+            proj["speedup_vs_classic"] = proj["classic_seconds"] / proj["seconds"]
     out = {"metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -273,7 +290,8 @@ def main():
                       "l2": "inputs 6.4 GB >> 126 MB L2, no flush needed"},
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak, "traffic": ncu_traffic(), "peak_source": peak_src,
-                        "kernel_ms": kern_ms, "bytes_per_cell": BYTES_PER_CELL},
+                        "kernel_ms": kern_ms, "bytes_per_cell": BYTES_PER_CELL,
+                        "classic_sweep_ms": classic_ms},
            "cpu_baseline": cpu,
            "e2e": e2e,
            "gpu_launches": args.steps * plan.launches_per_cycle_static,
