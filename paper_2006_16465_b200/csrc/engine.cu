@@ -310,9 +310,6 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
   g.tx = pr->mode == HJ_CLASSIC ? 1 : pr->tile_x;
   g.ty = pr->mode == HJ_CLASSIC ? 1 : pr->tile_y;
   g.k = pr->mode == HJ_CLASSIC ? 1 : pr->k;
-  if (const char* v = std::getenv("HJ_REG2D_VARIANT")) g.variant = std::atoi(v);
-  g.stagger_ns = 0;
-  if (const char* v = std::getenv("HJ_STAGGER_NS")) g.stagger_ns = std::atoi(v);
   hj_status s = choose_kernel(pb, pr, &g.kernel_kind);
   if (s != HJ_OK) { delete P; return s; }
   P->nsm = nsm;

@@ -82,8 +82,6 @@ struct Geom {
   int tx, ty, k;
   int ox, oy;                  // overlap along x / y (0: the paper's basic method)
   Axis ax, ay;                 // block plans (hierarchical modes)
-  int variant;                 // REG2D kernel variant (tuning knob, HJ_REG2D_VARIANT)
-  int stagger_ns;              // REG2D one-time per-warp start offset (HJ_STAGGER_NS)
   int64_t ntx, nty, ntiles;  // tiles of this plan (classic: row-blocks x col-blocks)
   int64_t parts_per_row;     // partials per row group (ntx; classic2d: 4 per CTA)
   int64_t nparts;            // number of residual partials

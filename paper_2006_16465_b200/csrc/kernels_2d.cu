@@ -30,9 +30,8 @@ template <> struct VecOf<float> { using v2 = float2; };
 // HBM traffic overlaps the k sub-iterations.  Persistent grid, 4 warps per SM sub-partition
 // multiple (8 f64 / 12 f32 warps per CTA, one CTA per SM).
 // =============================================================================
-template <typename T, int WARPS_ = (sizeof(T) == 8 ? 8 : 12), bool TMA_STORE_ = true, bool SAME_DIR_ = false>
+template <typename T, int WARPS_ = (sizeof(T) == 8 ? 8 : 12), bool TMA_STORE_ = true>
 struct R2 {
-  static constexpr bool SAME_DIR = SAME_DIR_;
   static constexpr int COL0 = 16 / sizeof(T);                          // interior column offset
   static constexpr int BW = ((COL0 + 33) + (16 / sizeof(T)) - 1) / (16 / sizeof(T)) * (16 / sizeof(T));
   static constexpr int BH = 34;
@@ -151,35 +150,6 @@ struct Tile2 {
     }
   }
 
-  // Ping-pong form: read src, write dst (no rolling row, no register renaming at the loop
-  // back-edge).  Used for the paired sub-iterations of the main loop.
-  __device__ __forceinline__ void sweep_pp(int lx, int ly, const T (&src)[8][4], T (&dst)[8][4]) const {
-    T up[4], dn[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      up[c] = __shfl_down_sync(FULL, src[0][c], 8);
-      dn[c] = __shfl_up_sync(FULL, src[7][c], 8);
-      const T hv = hyp[c];
-      up[c] = ly == 3 ? hv : up[c];
-      dn[c] = ly == 0 ? hv : dn[c];
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      T w = __shfl_up_sync(FULL, src[i][3], 1, 8);
-      T e = __shfl_down_sync(FULL, src[i][0], 1, 8);
-      const T hv = hxp[i];
-      w = lx == 0 ? hv : w;
-      e = lx == 7 ? hv : e;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const T W = c == 0 ? w : src[i][c - 1];
-        const T E = c == 3 ? e : src[i][c + 1];
-        const T S = i == 0 ? dn[c] : src[i - 1][c];
-        const T N = i == 7 ? up[c] : src[i + 1][c];
-        dst[i][c] = upd2(W, E, S, N, q[i][c]);
-      }
-    }
-  }
 };
 
 // One full 32x32 tile: smem slot -> registers, refill, fused residual, k sub-iterations, store.
@@ -235,30 +205,16 @@ __device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __
   }
   acc = warp_sum(acc);
   if (lane == 0) part[t] = acc;
-  // remaining sub-iterations, halo frozen
-  if constexpr (C::SAME_DIR) {
-    // register ping-pong: x -> y -> x per pair (variant 2)
-    if (s < kk && ((kk - s) & 1)) {
-      tl.template sweep<false>(lx, ly);
-      ++s;
-    }
-    T y[8][4];
+  // remaining sub-iterations, halo frozen; pairs of opposite-direction sweeps (the register
+  // names of the rolling row scheme rotate back after a pair)
+  if (s < kk && ((kk - s) & 1)) {
+    tl.template sweep<false>(lx, ly);
+    ++s;
+  }
 #pragma unroll 1
-    for (; s < kk; s += 2) {
-      tl.sweep_pp(lx, ly, tl.x, y);
-      tl.sweep_pp(lx, ly, y, tl.x);
-    }
-  } else {
-    // pairs of opposite-direction sweeps (register names rotate back after a pair)
-    if (s < kk && ((kk - s) & 1)) {
-      tl.template sweep<false>(lx, ly);
-      ++s;
-    }
-#pragma unroll 1
-    for (; s < kk; s += 2) {
-      tl.template sweep<true>(lx, ly);
-      tl.template sweep<false>(lx, ly);
-    }
+  for (; s < kk; s += 2) {
+    tl.template sweep<true>(lx, ly);
+    tl.template sweep<false>(lx, ly);
   }
   if (kk == 0) return;  // residual-only pass (after max_cycles)
   if constexpr (MASK) {
@@ -300,7 +256,7 @@ __global__ void __launch_bounds__(C::WARPS * 32, 1)
 reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
              const __grid_constant__ CUtensorMap tmO, T* __restrict__ xout, long long pitch,
              Axis ax, Axis ay, int ntx_full, long long nfull, int ntx, double* __restrict__ part,
-             const Ctrl* __restrict__ ctrl, int k, long long max_cycles, int stagger_ns) {
+             const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
   extern __shared__ unsigned char smem_raw[];
@@ -331,10 +287,6 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
     issue(gw);
   }
   __syncwarp();
-  // De-phase the warps of an SM once per launch: with fair bandwidth sharing, warps that start
-  // together receive their tiles together and stay phase-locked (memory bursts, then idle HBM
-  // while everyone computes).  A one-time offset of warp * stagger spreads the refills.
-  if (stagger_ns > 0 && warp > 0) __nanosleep((unsigned)(warp * stagger_ns));
   int it = 0;
   for (long long u = gw; u < nfull; u += nw, ++it) {
     mbar_wait(bar, it & 1);
@@ -545,10 +497,9 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
         if (ctas > grid_hint) ctas = grid_hint;
         reg2d_kernel<T, C, decltype(mask)::value><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
             *a.tm_in, *a.tm_f, *a.tm_out, (T*)a.xout, g.pitch, g.ax, g.ay, (int)ntx_full, nfull,
-            (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles, g.stagger_ns);
+            (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles);
       };
       if (ovl) go(R2<T>{}, std::true_type{});
-      else if (g.variant == 2) go(R2<T, (sizeof(T) == 8 ? 8 : 12), true, true>{}, std::false_type{});
       else go(R2<T>{}, std::false_type{});
     }
     const long long nedge = g.ntiles - nfull;
@@ -582,8 +533,6 @@ cudaError_t cfg2() {
 cudaError_t configure_2d() {
   cudaError_t e;
   if ((e = cfg2<double, R2<double>>()) != cudaSuccess) return e;
-  if ((e = cfg2<double, R2<double, 8, true, true>>()) != cudaSuccess) return e;
-  if ((e = cfg2<float, R2<float, 12, true, true>>()) != cudaSuccess) return e;
   if ((e = cfg2<float, R2<float>>()) != cudaSuccess) return e;
   e = cudaFuncSetAttribute(smem2d_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return e;

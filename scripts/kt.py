@@ -20,7 +20,7 @@ def run(n=16384, k=16, mode="hier", dtype="f64", kernel="auto", steps=20):
     ms = e0.elapsed_time(e1) / steps
     kms = km / steps
     cells = n * n
-    out = dict(n=n, k=k, mode=mode, dtype=dtype, kernel=kernel, variant=os.environ.get("HJ_REG2D_VARIANT", "0"),
+    out = dict(n=n, k=k, mode=mode, dtype=dtype, kernel=kernel,
                ms_cycle=round(ms, 4), ms_kernel=round(kms, 4),
                gbs=round((24 if dtype == "f64" else 12) * cells / kms / 1e6, 1),
                gupd=round(cells * (k if mode == "hier" else 1) / kms / 1e6, 1))
