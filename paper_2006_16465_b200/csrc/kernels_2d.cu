@@ -108,21 +108,20 @@ struct Tile2 {
     return acc;
   }
 
-  // One Jacobi sub-iteration, rows processed top-down (DOWN) or bottom-up, keeping only
-  // one saved old row; alternating directions lets the register allocator rotate names.
-  // RES (f64 only): also accumulate the snapshot residual from the same neighbour sums:
-  // s = h2f - (4x - ((W+E)+(S+N))) with h2f = 4q and 4x exact, so two fmas give the oracle's
-  // bits: t = fma(4, x, -sum) = 4x - sum,  s = fma(4, q, -t) = h2f - t.
-  template <bool DOWN, bool RES = false>
-  __device__ __forceinline__ void sweep(int lx, int ly, double* acc = nullptr) {  // acc[4]
+  // One Jacobi sub-iteration in middle-out row order 3,4,2,5,1,6,0,7: every row's inputs from the
+  // previous sub-iteration were produced >= 3 rows earlier, and the cross-lane N/S values (rows 0
+  // and 7 of the neighbouring lane rows) are consumed last, so consecutive sub-iterations overlap
+  // instead of draining the pipeline.  The computed rows form a growing block [lo, hi]; the old
+  // values of its two edge rows are kept in olo / ohi.
+  template <bool RES = false>
+  __device__ __forceinline__ void sweep_mo(int lx, int ly, double* acc = nullptr) {
     T up[4], dn[4];
     exchange_ns(ly, up, dn);
-    T saved[4];
+    T olo[4], ohi[4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) saved[c] = DOWN ? dn[c] : up[c];
-#pragma unroll
-    for (int ii = 0; ii < 8; ++ii) {
-      const int i = DOWN ? ii : 7 - ii;
+    for (int step = 0; step < 8; ++step) {
+      const int i = step == 0 ? 3 : (step & 1) ? 3 + (step + 1) / 2 : 3 - step / 2;  // 3,4,2,5,1,6,0,7
+      const bool hi_side = step > 0 && (step & 1);
       T w, e;
       exchange_we(lx, i, w, e);
       T nw[4];
@@ -130,8 +129,9 @@ struct Tile2 {
       for (int c = 0; c < 4; ++c) {
         const T W = c == 0 ? w : x[i][c - 1];
         const T E = c == 3 ? e : x[i][c + 1];
-        const T S = DOWN ? saved[c] : (i == 0 ? dn[c] : x[i - 1][c]);
-        const T N = DOWN ? (i == 7 ? up[c] : x[i + 1][c]) : saved[c];
+        // S = old row i-1, N = old row i+1
+        const T S = (i == 0) ? dn[c] : (step > 0 && hi_side ? ohi[c] : x[i - 1][c]);
+        const T N = (i == 7) ? up[c] : (step > 0 && !hi_side ? olo[c] : x[i + 1][c]);
         if constexpr (RES) {
           const double sum = __dadd_rn(__dadd_rn(W, E), __dadd_rn(S, N));
           nw[c] = __fma_rn(0.25, sum, q[i][c]);
@@ -144,7 +144,9 @@ struct Tile2 {
       }
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        saved[c] = x[i][c];
+        if (step == 0) { olo[c] = x[i][c]; ohi[c] = x[i][c]; }
+        else if (hi_side) ohi[c] = x[i][c];
+        else olo[c] = x[i][c];
         x[i][c] = nw[c];
       }
     }
@@ -199,22 +201,21 @@ __device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __
   int s = 0;
   if (FOLD && kk > 0) {
     double a4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent accumulation chains
-    tl.template sweep<true, true>(lx, ly, a4);
+    tl.template sweep_mo<true>(lx, ly, a4);
     acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
     s = 1;
   }
   acc = warp_sum(acc);
   if (lane == 0) part[t] = acc;
-  // remaining sub-iterations, halo frozen; pairs of opposite-direction sweeps (the register
-  // names of the rolling row scheme rotate back after a pair)
+  // remaining sub-iterations, halo frozen
   if (s < kk && ((kk - s) & 1)) {
-    tl.template sweep<false>(lx, ly);
+    tl.template sweep_mo<false>(lx, ly);
     ++s;
   }
 #pragma unroll 1
   for (; s < kk; s += 2) {
-    tl.template sweep<true>(lx, ly);
-    tl.template sweep<false>(lx, ly);
+    tl.template sweep_mo<false>(lx, ly);
+    tl.template sweep_mo<false>(lx, ly);
   }
   if (kk == 0) return;  // residual-only pass (after max_cycles)
   if constexpr (MASK) {
