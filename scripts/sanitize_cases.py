@@ -18,9 +18,12 @@ cases = [
     (2, 128, 64, dict(mode="hier", tile=(32, 32), k=4, overlap=8, dtype="f32")),
     (2, 96, 64, dict(mode="hier", tile=(32, 32), k=4, overlap=2, dtype="f32")),
     (1, 1000, 1, dict(mode="hier", tile=64, k=7, overlap=10)),         # overlapping blocks, smem1d
+    (1, 1024, 9, dict(mode="hier", tile=32, k=16)),                     # batched 1D, reg1d
+    (1, 1000, 5, dict(mode="hier", tile=96, k=3)),                      # batched 1D, smem1d
+    (1, 3000, 4, dict(mode="classic")),                                 # batched 1D, classic
 ]
 for dim, nx, ny, kw in cases:
-    p = make_problem("R", dim, nx, ny)
+    p = make_problem("R", dim, nx, ny) if (dim == 2 or ny == 1) else make_problem("R", 1, nx, batch=ny)
     r = hj.jacobi_solve(dim, nx, ny, p["h"], p["f"], p["bc"], p["x0"], tol=1e-9, max_cycles=6, **kw)
     print(dim, nx, ny, kw, "cycles", r["cycles"], "status", r["status"])
 print("sanitize cases done")
