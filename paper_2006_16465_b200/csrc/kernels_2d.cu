@@ -30,7 +30,7 @@ template <> struct VecOf<float> { using v2 = float2; };
 // HBM traffic overlaps the k sub-iterations.  Persistent grid, 4 warps per SM sub-partition
 // multiple (8 f64 / 12 f32 warps per CTA, one CTA per SM).
 // =============================================================================
-template <typename T, int WARPS_ = (sizeof(T) == 8 ? 8 : 12), bool TMA_STORE_ = true>
+template <typename T, int WARPS_ = (sizeof(T) == 8 ? 8 : 12), bool TMA_STORE_ = false>
 struct R2 {
   static constexpr int COL0 = 16 / sizeof(T);                          // interior column offset
   static constexpr int BW = ((COL0 + 33) + (16 / sizeof(T)) - 1) / (16 / sizeof(T)) * (16 / sizeof(T));
@@ -529,6 +529,11 @@ cudaError_t cfg2() {
                                        (int)C::SMEM);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(reg2d_kernel<T, C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+}
+
+template <typename T, typename C>
+cudaError_t cfg2u() {  // unmasked instantiation only
+  return cudaFuncSetAttribute(reg2d_kernel<T, C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
 }
 
 cudaError_t configure_2d() {
