@@ -52,12 +52,15 @@ def _load():
             d, i64, i32 = ctypes.c_double, ctypes.c_int64, ctypes.c_int
             P = ctypes.c_void_p
             lib.hjo_solve.restype = i32
-            lib.hjo_solve.argtypes = [i32, i64, i64, d, P, P, P, i32, i32, i64, i64, i64, i64, i32, d,
-                                      i32, d, i64, i32, P, P, ctypes.POINTER(i64), ctypes.POINTER(i32)]
+            lib.hjo_solve.argtypes = [i32, i64, i64, d, P, P, P, P, i32, i32, i64, i64, i64, i64, i32,
+                                      d, i32, d, i64, i32, P, P, ctypes.POINTER(i64),
+                                      ctypes.POINTER(i32)]
             lib.hjo_block_plan.restype = i64
             lib.hjo_block_plan.argtypes = [i64, i64, i64, i64, P, P, P, P]
             lib.hjo_residual.restype = d
             lib.hjo_residual.argtypes = [i32, i64, i64, d, P, P, P]
+            lib.hjo_residual_general.restype = d
+            lib.hjo_residual_general.argtypes = [i32, i64, i64, P, P, P, P]
             lib.hjo_resource_figures.restype = i32
             lib.hjo_resource_figures.argtypes = [i32, i64, i64, i64, i64, i64, i64, i64,
                                                  ctypes.POINTER(i64), ctypes.POINTER(i64),
@@ -81,10 +84,12 @@ def _f64(a, n, name):
 
 def solve(dim, nx, ny, h, f, bc=None, x0=None, *, mode="hier", dtype="f64", tile=(32, 32), k=16,
           overlap=0, tol=1e-4, tol_mode="rel", ref_residual=0.0, max_cycles=10**7, tile_order=0,
-          history=True):
+          history=True, stencil=None):
     """Run the oracle solver.  Returns dict(x, history, cycles, converged, status).
 
     ``x`` has shape (ny, nx) in 2D and (nx,) in 1D; ``history[c]`` = ||f - A x_c||_2.
+    ``stencil`` (general coefficients, reading c23): 2D {a, c, e, f, d} (Eq. 10), 1D the planes
+    [a | d | c] of nx*ny values each (Eq. 4); ``f`` is then b and ``h`` is unused.
     ``max_cycles`` cycles are run if ``tol`` is never met (``tol=0`` runs exactly
     ``max_cycles`` cycles unless the residual is exactly zero).
     """
@@ -94,13 +99,15 @@ def solve(dim, nx, ny, h, f, bc=None, x0=None, *, mode="hier", dtype="f64", tile
     nbc = 2 * ny if dim == 1 else 2 * nx + 2 * ny   # dim 1: ny independent problems
     bc = _f64(bc, nbc, "bc")
     x0 = _f64(x0, n, "x0")
+    if stencil is not None:
+        stencil = _f64(stencil, 3 * n if dim == 1 else 5, "stencil")
     x = np.zeros(n, dtype=np.float64)
     hist = np.full(max_cycles + 1, np.nan) if history else None
     cyc = ctypes.c_int64(0)
     conv = ctypes.c_int(0)
     tx, ty = (tile if isinstance(tile, (tuple, list)) else (tile, 1))
     ox, oy = (overlap if isinstance(overlap, (tuple, list)) else (overlap, overlap if dim == 2 else 0))
-    st = lib.hjo_solve(dim, nx, ny, float(h), _ptr(f), _ptr(bc), _ptr(x0),
+    st = lib.hjo_solve(dim, nx, ny, float(h), _ptr(f), _ptr(bc), _ptr(x0), _ptr(stencil),
                        {"hier": 0, "classic": 1}[mode], {"f64": 0, "f32": 1}[dtype], tx, ty, ox, oy, k,
                        float(tol), {"rel": 0, "abs": 1}[tol_mode], float(ref_residual),
                        int(max_cycles), int(tile_order), _ptr(x), _ptr(hist),
@@ -121,6 +128,17 @@ def residual(dim, nx, ny, h, f, bc, x):
     x = _f64(x, n, "x")
     bc = _f64(bc, 2 * ny if dim == 1 else 2 * nx + 2 * ny, "bc")
     return lib.hjo_residual(dim, nx, ny, float(h), _ptr(f), _ptr(bc), _ptr(x))
+
+
+def residual_general(dim, nx, ny, f, bc, x, stencil):
+    """General-coefficient residual by its definition: 2D ||b - Ax||_2, 1D ||D^-1 (b - Ax)||_2."""
+    lib = _load()
+    n = nx * ny
+    f = _f64(f, n, "f")
+    x = _f64(x, n, "x")
+    bc = _f64(bc, 2 * ny if dim == 1 else 2 * nx + 2 * ny, "bc")
+    stencil = _f64(stencil, 3 * n if dim == 1 else 5, "stencil")
+    return lib.hjo_residual_general(dim, nx, ny, _ptr(f), _ptr(bc), _ptr(x), _ptr(stencil))
 
 
 def resource_figures(dim, nx, ny, tx, ty=1, bytes_per_value=8, overlap=0):

@@ -40,6 +40,17 @@
 //       (c16: keeps fp32 at 12 B/cell; differs from the true rhs by
 //       at most one fp32 rounding of h^2 f, far below the fp32 residual floor).
 //
+// General coefficients (reading c23): the tridiagonal update of
+// Eq. 4 with per-point a_i, d_i, c_i and the pentadiagonal update of Eq. 10
+// with constants a, c, e, f, d, evaluated as
+//       1D: fma(wR, xR, fma(wL, xL, q))                       wL = T(-a_i/d_i), wR = T(-c_i/d_i)
+//       2D: fma(wN, xN, fma(wS, xS, fma(wE, xE, fma(wW, xW, q))))   wW = T(-a/d), wE = T(-c/d),
+//                                                              wS = T(-e/d), wN = T(-f/d)
+//       q = T(b/d) (b = the f array, NOT scaled by h^2; h is unused)
+// (the division of Eq. 4/10 distributed over the terms, each quotient rounded once to T).  The
+// residual is the Jacobi-scaled s = D^{-1}(b - Ax) = (same chain in double) - x, summed as s^2;
+// the reported norm is ||s|| * |d| in 2D (= ||b - Ax||, d constant) and ||s|| in 1D (d_i varies).
+//
 // Canonical arithmetic: the elemental update of
 // PAPER.md:210 / :420 is evaluated exactly as
 //       1D: T(0.5)  * ((xL + xR) + h2f)
@@ -122,12 +133,26 @@ inline double resid1d(double x, double left, double right, double h2f64) {
   return h2f64 - (2.0 * x - (left + right));
 }
 
+// General tridiagonal update, Eq. 4: x_i <- (b_i - a_i x_{i-1} - c_i x_{i+1}) / d_i
+// with the division distributed (reading c23): q + wL x_{i-1} + wR x_{i+1}, two fused
+// multiply-adds in T.
+template <typename T>
+inline T update1d_gen(T wl, T wr, T left, T right, T q) {
+  return std::fma(wr, right, std::fma(wl, left, q));
+}
+// D^{-1}(b - Ax) at one point, in double from the T weights and q (reading c23).
+inline double resid1d_gen(double wl, double wr, double x, double left, double right, double q) {
+  return std::fma(wr, right, std::fma(wl, left, q)) - x;
+}
+
 template <typename T>
 struct Problem1D {
   int64_t n;                 // interior points (paper's N)
   double h2;                 // h*h
-  std::vector<T> h2f;        // T(h2*f_i), i = 0..n-1 (interior index)
-  std::vector<double> h2f64; // double(h2f_i): rhs used by the residual (c16)
+  bool gen = false;          // general coefficients (Eq. 4) instead of -u'' = f
+  std::vector<T> h2f;        // Poisson: T(h2*f_i), i = 0..n-1; general: q_i = T(b_i/d_i)
+  std::vector<double> h2f64; // Poisson: double(h2f_i), rhs used by the residual (c16)
+  std::vector<T> wl, wr;     // general: T(-a_i/d_i), T(-c_i/d_i)
   T gl, gr;                  // Dirichlet values at x=0 and x=1
 };
 
@@ -136,7 +161,9 @@ template <typename T>
 double residual_sq_1d(const Problem1D<T>& p, const std::vector<T>& x) {
   double S = 0.0;
   for (int64_t i = 1; i <= p.n; ++i) {
-    double s = resid1d((double)x[i], (double)x[i - 1], (double)x[i + 1], p.h2f64[i - 1]);
+    double s = p.gen ? resid1d_gen((double)p.wl[i - 1], (double)p.wr[i - 1], (double)x[i],
+                                   (double)x[i - 1], (double)x[i + 1], (double)p.h2f[i - 1])
+                     : resid1d((double)x[i], (double)x[i - 1], (double)x[i + 1], p.h2f64[i - 1]);
     S += s * s;
   }
   return S;
@@ -146,7 +173,8 @@ double residual_sq_1d(const Problem1D<T>& p, const std::vector<T>& x) {
 template <typename T>
 void classic_sweep_1d(const Problem1D<T>& p, const std::vector<T>& x0, std::vector<T>& x1) {
   for (int64_t i = 1; i <= p.n; ++i)
-    x1[i] = update1d<T>(x0[i - 1], x0[i + 1], p.h2f[i - 1]);
+    x1[i] = p.gen ? update1d_gen<T>(p.wl[i - 1], p.wr[i - 1], x0[i - 1], x0[i + 1], p.h2f[i - 1])
+                  : update1d<T>(x0[i - 1], x0[i + 1], p.h2f[i - 1]);
 }
 
 // §3.3 hierarchical cycle, 1D (Appendix A :548-573), blocks from block_plan.
@@ -156,7 +184,7 @@ template <typename T>
 void hier_cycle_1d(const Problem1D<T>& p, const BlockPlan& bp, int k, int tile_order,
                    const std::vector<T>& xc, std::vector<T>& xn) {
   const int64_t nb = (int64_t)bp.start.size();
-  std::vector<T> A, B, rhs;
+  std::vector<T> A, B, rhs, wl, wr;
   for (int64_t tt = 0; tt < nb; ++tt) {
     const int64_t t = tile_order == 0 ? tt : nb - 1 - tt;
     const int64_t lo = bp.start[t];        // first interior point of the subdomain
@@ -167,10 +195,16 @@ void hier_cycle_1d(const Problem1D<T>& p, const BlockPlan& bp, int k, int tile_o
     A.assign(xc.begin() + (lo - 1), xc.begin() + (hi + 2));
     B = A;
     rhs.assign(p.h2f.begin() + (lo - 1), p.h2f.begin() + hi);
+    if (p.gen) {  // the block's coefficients travel with its rhs (reading c23)
+      wl.assign(p.wl.begin() + (lo - 1), p.wl.begin() + hi);
+      wr.assign(p.wr.begin() + (lo - 1), p.wr.begin() + hi);
+    }
     // Step 2: k sub-iterations on the interior; the two halo points are never
     // written (frozen at snapshot values, reading c5).
     for (int q = 0; q < k; ++q) {
-      for (int64_t i = 1; i <= w; ++i) B[i] = update1d<T>(A[i - 1], A[i + 1], rhs[i - 1]);
+      for (int64_t i = 1; i <= w; ++i)
+        B[i] = p.gen ? update1d_gen<T>(wl[i - 1], wr[i - 1], A[i - 1], A[i + 1], rhs[i - 1])
+                     : update1d<T>(A[i - 1], A[i + 1], rhs[i - 1]);
       std::swap(A, B);
     }
     // Step 3: write the latest values of the OWNED points into the NEXT global array
@@ -192,13 +226,31 @@ inline double resid2d(double x, double w, double e, double s, double n, double h
   return h2f64 - (4.0 * x - ((w + e) + (s + n)));
 }
 
+// General pentadiagonal update, Eq. 10:
+//   x_ij <- (b_ij - a x_{i-1,j} - c x_{i+1,j} - e x_{i,j-1} - f x_{i,j+1}) / d
+// with the division distributed (reading c23): four fused multiply-adds in T, W, E, S, N order.
+template <typename T>
+inline T update2d_gen(const T* wt, T w, T e, T s, T n, T q) {
+  return std::fma(wt[3], n, std::fma(wt[2], s, std::fma(wt[1], e, std::fma(wt[0], w, q))));
+}
+template <typename T>
+inline double resid2d_gen(const T* wt, double x, double w, double e, double s, double n, double q) {
+  return std::fma((double)wt[3], n,
+                  std::fma((double)wt[2], s, std::fma((double)wt[1], e, std::fma((double)wt[0], w, q)))) - x;
+}
+
 template <typename T>
 struct Problem2D {
   int64_t nx, ny;
   double h2;
-  std::vector<T> h2f;        // nx*ny, row-major
+  bool gen = false;          // general constant coefficients (Eq. 10) instead of -Δu = f
+  T wt[4] = {T(0), T(0), T(0), T(0)};  // general: T(-a/d), T(-c/d), T(-e/d), T(-f/d)  (W, E, S, N)
+  std::vector<T> h2f;        // nx*ny, row-major: Poisson T(h2*f); general q = T(b/d)
   std::vector<double> h2f64; // nx*ny, double(h2f) (c16)
   int64_t pitch() const { return nx + 2; }
+  T upd(T w, T e, T s, T n, T q) const {
+    return gen ? update2d_gen<T>(wt, w, e, s, n, q) : update2d<T>(w, e, s, n, q);
+  }
 };
 
 // index of (i, j) in a ringed grid, i = 0..nx+1 (x), j = 0..ny+1 (y)
@@ -210,9 +262,11 @@ double residual_sq_2d(const Problem2D<T>& p, const std::vector<T>& x) {
   double S = 0.0;
   for (int64_t j = 1; j <= p.ny; ++j)
     for (int64_t i = 1; i <= p.nx; ++i) {
-      double s = resid2d((double)x[at(p, i, j)], (double)x[at(p, i - 1, j)], (double)x[at(p, i + 1, j)],
-                         (double)x[at(p, i, j - 1)], (double)x[at(p, i, j + 1)],
-                         p.h2f64[(j - 1) * p.nx + (i - 1)]);
+      const double xc = (double)x[at(p, i, j)], w = (double)x[at(p, i - 1, j)],
+                   e = (double)x[at(p, i + 1, j)], so = (double)x[at(p, i, j - 1)],
+                   no = (double)x[at(p, i, j + 1)];
+      double s = p.gen ? resid2d_gen<T>(p.wt, xc, w, e, so, no, (double)p.h2f[(j - 1) * p.nx + (i - 1)])
+                       : resid2d(xc, w, e, so, no, p.h2f64[(j - 1) * p.nx + (i - 1)]);
       S += s * s;
     }
   return S;
@@ -222,8 +276,8 @@ template <typename T>
 void classic_sweep_2d(const Problem2D<T>& p, const std::vector<T>& x0, std::vector<T>& x1) {
   for (int64_t j = 1; j <= p.ny; ++j)
     for (int64_t i = 1; i <= p.nx; ++i)
-      x1[at(p, i, j)] = update2d<T>(x0[at(p, i - 1, j)], x0[at(p, i + 1, j)], x0[at(p, i, j - 1)],
-                                    x0[at(p, i, j + 1)], p.h2f[(j - 1) * p.nx + (i - 1)]);
+      x1[at(p, i, j)] = p.upd(x0[at(p, i - 1, j)], x0[at(p, i + 1, j)], x0[at(p, i, j - 1)],
+                              x0[at(p, i, j + 1)], p.h2f[(j - 1) * p.nx + (i - 1)]);
 }
 
 // §4.1 hierarchical cycle, 2D.  Block (a, b) = x-block a of bx times y-block b
@@ -254,8 +308,8 @@ void hier_cycle_2d(const Problem2D<T>& p, const BlockPlan& bx, const BlockPlan& 
     for (int q = 0; q < k; ++q) {
       for (int64_t jj = 1; jj <= hgt; ++jj)
         for (int64_t ii = 1; ii <= w; ++ii)
-          B[jj * lp + ii] = update2d<T>(A[jj * lp + ii - 1], A[jj * lp + ii + 1], A[(jj - 1) * lp + ii],
-                                        A[(jj + 1) * lp + ii], rhs[(jj - 1) * w + (ii - 1)]);
+          B[jj * lp + ii] = p.upd(A[jj * lp + ii - 1], A[jj * lp + ii + 1], A[(jj - 1) * lp + ii],
+                                  A[(jj + 1) * lp + ii], rhs[(jj - 1) * w + (ii - 1)]);
       std::swap(A, B);
     }
     // Step 3: write the owned points into the next global array.
@@ -266,10 +320,11 @@ void hier_cycle_2d(const Problem2D<T>& p, const BlockPlan& bx, const BlockPlan& 
 }
 
 // ------------------------------------------------------------- driver ---------
-// SURVEY.md §8(c) step 6.  S_0 = S(x_0) (or (ref_residual*h2)^2).  hist[0].
+// SURVEY.md §8(c) step 6.  S_0 = S(x_0) (or (ref_residual*rdiv)^2).  hist[0].
 // If S_0 == 0 return c = 0.  For c = 1..max_cycles: x_c, S_c, hist[c];
 // non-finite -> status 4; sqrt(S_c) <= tol*sqrt(S_0) -> converged at c.
-// Absolute mode: sqrt(S_c)/h2 <= tol.
+// Absolute mode: sqrt(S_c)/rdiv <= tol.  rdiv converts the summed scaled residual into the
+// reported norm: h^2 (Poisson, c3), 1/|d| (general 2D), 1 (general 1D) — reading c23.
 
 enum { ST_OK = 0, ST_NOT_CONVERGED = 1, ST_INVALID = 2, ST_NUMERIC = 4 };
 
@@ -280,15 +335,15 @@ struct DriverOut {
 };
 
 template <typename Cycle, typename Resid>
-DriverOut drive(double h2, double tol, int tol_mode, double ref_residual, int64_t max_cycles,
+DriverOut drive(double rdiv, double tol, int tol_mode, double ref_residual, int64_t max_cycles,
                 double* hist, Cycle&& cycle, Resid&& resid) {
   DriverOut out;
   double S0 = resid();
-  double sqrtS0 = ref_residual > 0.0 ? ref_residual * h2 : std::sqrt(S0);
-  if (hist) hist[0] = std::sqrt(S0) / h2;
+  double sqrtS0 = ref_residual > 0.0 ? ref_residual * rdiv : std::sqrt(S0);
+  if (hist) hist[0] = std::sqrt(S0) / rdiv;
   if (!std::isfinite(S0)) { out.status = ST_NUMERIC; return out; }
   auto test = [&](double S) {
-    return tol_mode == 0 ? (std::sqrt(S) <= tol * sqrtS0) : (std::sqrt(S) / h2 <= tol);
+    return tol_mode == 0 ? (std::sqrt(S) <= tol * sqrtS0) : (std::sqrt(S) / rdiv <= tol);
   };
   if (S0 == 0.0 || (ref_residual > 0.0 && test(S0)) || (tol_mode == 1 && test(S0))) {
     out.converged = 1;
@@ -298,7 +353,7 @@ DriverOut drive(double h2, double tol, int tol_mode, double ref_residual, int64_
   for (int64_t c = 1; c <= max_cycles; ++c) {
     cycle();
     double S = resid();
-    if (hist) hist[c] = std::sqrt(S) / h2;
+    if (hist) hist[c] = std::sqrt(S) / rdiv;
     out.cycles = c;
     if (!std::isfinite(S)) { out.status = ST_NUMERIC; return out; }
     if (test(S)) { out.converged = 1; return out; }
@@ -310,21 +365,37 @@ DriverOut drive(double h2, double tol, int tol_mode, double ref_residual, int64_
 // B independent 1D problems (the paper's "1024 copies"):
 // problem b has interior f[b*n .. b*n+n), ends bc[2b], bc[2b+1]; one cycle advances every problem;
 // the stopping test uses the L2 norm of the stacked residual (sum over problems in order).
+// stencil (general coefficients, Eq. 4) = NULL or three planes of n*batch doubles:
+// [a (sub-diagonal) | d (diagonal) | c (super-diagonal)], point i of problem b at b*n + i.
 template <typename T>
 int solve1d(int64_t n, int64_t batch, double h, const double* f, const double* bc, const double* x0,
-            int mode, int64_t tile, int64_t overlap, int k, double tol, int tol_mode,
-            double ref_residual, int64_t max_cycles, int tile_order, double* x_out, double* hist,
-            int64_t* cycles, int* converged) {
+            const double* stencil, int mode, int64_t tile, int64_t overlap, int k, double tol,
+            int tol_mode, double ref_residual, int64_t max_cycles, int tile_order, double* x_out,
+            double* hist, int64_t* cycles, int* converged) {
   std::vector<Problem1D<T>> ps(batch);
   std::vector<std::vector<T>> xa(batch), xb(batch);
+  const int64_t nt = n * batch;
   for (int64_t b = 0; b < batch; ++b) {
     Problem1D<T>& p = ps[b];
     p.n = n;
     p.h2 = h * h;
+    p.gen = stencil != nullptr;
     p.h2f.resize(n);
     p.h2f64.resize(n);
+    if (p.gen) {
+      p.wl.resize(n);
+      p.wr.resize(n);
+    }
     for (int64_t i = 0; i < n; ++i) {
-      p.h2f[i] = (T)(p.h2 * f[b * n + i]);
+      const int64_t g = b * n + i;
+      if (p.gen) {  // reading c23: q = T(b/d), wL = T(-a/d), wR = T(-c/d)
+        const double a = stencil[g], d = stencil[nt + g], c = stencil[2 * nt + g];
+        p.h2f[i] = (T)(f[g] / d);
+        p.wl[i] = (T)(-a / d);
+        p.wr[i] = (T)(-c / d);
+      } else {
+        p.h2f[i] = (T)(p.h2 * f[g]);
+      }
       p.h2f64[i] = (double)p.h2f[i];  // reading c16: residual of the rounded system
     }
     xa[b].assign(n + 2, T(0));
@@ -349,7 +420,7 @@ int solve1d(int64_t n, int64_t batch, double h, const double* f, const double* b
     for (int64_t b = 0; b < batch; ++b) S += residual_sq_1d(ps[b], flip ? xb[b] : xa[b]);
     return S;
   };
-  DriverOut o = drive(h * h, tol, tol_mode, ref_residual, max_cycles, hist, cycle, resid);
+  DriverOut o = drive(stencil ? 1.0 : h * h, tol, tol_mode, ref_residual, max_cycles, hist, cycle, resid);
   for (int64_t b = 0; b < batch; ++b)
     for (int64_t i = 0; i < n; ++i) x_out[b * n + i] = (double)(flip ? xb[b] : xa[b])[i + 1];
   *cycles = o.cycles;
@@ -357,19 +428,28 @@ int solve1d(int64_t n, int64_t batch, double h, const double* f, const double* b
   return o.status;
 }
 
+// stencil (general constant coefficients, Eq. 10) = NULL or {a, c, e, f, d}: the coefficients of
+// x_{i-1,j} (west), x_{i+1,j} (east), x_{i,j-1} (south), x_{i,j+1} (north) and x_{ij}.
 template <typename T>
 int solve2d(int64_t nx, int64_t ny, double h, const double* f, const double* bc, const double* x0,
-            int mode, int64_t tx, int64_t ty, int64_t ox, int64_t oy, int k, double tol, int tol_mode,
-            double ref_residual, int64_t max_cycles, int tile_order, double* x_out, double* hist,
-            int64_t* cycles, int* converged) {
+            const double* stencil, int mode, int64_t tx, int64_t ty, int64_t ox, int64_t oy, int k,
+            double tol, int tol_mode, double ref_residual, int64_t max_cycles, int tile_order,
+            double* x_out, double* hist, int64_t* cycles, int* converged) {
   Problem2D<T> p;
   p.nx = nx;
   p.ny = ny;
   p.h2 = h * h;
+  p.gen = stencil != nullptr;
   p.h2f.resize(nx * ny);
   p.h2f64.resize(nx * ny);
+  double rdiv = p.h2;
+  if (p.gen) {  // reading c23
+    const double d = stencil[4];
+    for (int q = 0; q < 4; ++q) p.wt[q] = (T)(-stencil[q] / d);
+    rdiv = 1.0 / std::fabs(d);
+  }
   for (int64_t q = 0; q < nx * ny; ++q) {
-    p.h2f[q] = (T)(p.h2 * f[q]);
+    p.h2f[q] = p.gen ? (T)(f[q] / stencil[4]) : (T)(p.h2 * f[q]);
     p.h2f64[q] = (double)p.h2f[q];  // reading c16: residual of the rounded system
   }
   std::vector<T> xa((nx + 2) * (ny + 2), T(0));
@@ -397,7 +477,7 @@ int solve2d(int64_t nx, int64_t ny, double h, const double* f, const double* bc,
     std::swap(cur, nxt);
   };
   auto resid = [&]() { return residual_sq_2d(p, *cur); };
-  DriverOut o = drive(p.h2, tol, tol_mode, ref_residual, max_cycles, hist, cycle, resid);
+  DriverOut o = drive(rdiv, tol, tol_mode, ref_residual, max_cycles, hist, cycle, resid);
   for (int64_t j = 1; j <= ny; ++j)
     for (int64_t i = 1; i <= nx; ++i) x_out[(j - 1) * nx + (i - 1)] = (double)(*cur)[at(p, i, j)];
   *cycles = o.cycles;
@@ -415,32 +495,46 @@ extern "C" {
 // x_out: nx*ny doubles.  hist: max_cycles+1 doubles or NULL.
 // Returns 0 converged, 1 not converged, 2 invalid argument, 4 non-finite residual.
 // overlap_x/overlap_y: the paper's o (even, 0 <= o < tile).
+// stencil: NULL (Poisson) or the general coefficients (see solve1d / solve2d; reading c23);
+// every d must be finite and non-zero.
 int hjo_solve(int dim, int64_t nx, int64_t ny, double h, const double* f, const double* bc,
-              const double* x0, int mode, int dtype, int64_t tile_x, int64_t tile_y,
-              int64_t overlap_x, int64_t overlap_y, int k, double tol, int tol_mode,
+              const double* x0, const double* stencil, int mode, int dtype, int64_t tile_x,
+              int64_t tile_y, int64_t overlap_x, int64_t overlap_y, int k, double tol, int tol_mode,
               double ref_residual, int64_t max_cycles, int tile_order, double* x_out, double* hist,
               int64_t* cycles, int* converged) {
   if (!f || !x_out || !cycles || !converged) return ST_INVALID;
-  if (!(h > 0.0) || !std::isfinite(h) || nx < 1 || ny < 1 || max_cycles < 0) return ST_INVALID;
+  if (nx < 1 || ny < 1 || max_cycles < 0) return ST_INVALID;
+  if (!stencil && (!(h > 0.0) || !std::isfinite(h))) return ST_INVALID;
+  if (stencil) {
+    const int64_t ns = dim == 1 ? 3 * nx * ny : 5;
+    for (int64_t q = 0; q < ns; ++q)
+      if (!std::isfinite(stencil[q])) return ST_INVALID;
+    if (dim == 1) {
+      for (int64_t q = 0; q < nx * ny; ++q)
+        if (stencil[nx * ny + q] == 0.0) return ST_INVALID;
+    } else if (stencil[4] == 0.0) {
+      return ST_INVALID;
+    }
+  }
   if (mode != 0 && mode != 1) return ST_INVALID;
   if (mode == 0 && (k < 1 || tile_x < 1 || tile_x > nx)) return ST_INVALID;
   if (mode == 0 && (overlap_x < 0 || overlap_x % 2 != 0 || overlap_x >= tile_x)) return ST_INVALID;
   if (dim == 1) {  // ny = number of independent problems (batch)
     if (dtype == 0)
-      return solve1d<double>(nx, ny, h, f, bc, x0, mode, tile_x, overlap_x, k, tol, tol_mode,
+      return solve1d<double>(nx, ny, h, f, bc, x0, stencil, mode, tile_x, overlap_x, k, tol, tol_mode,
                              ref_residual, max_cycles, tile_order, x_out, hist, cycles, converged);
-    return solve1d<float>(nx, ny, h, f, bc, x0, mode, tile_x, overlap_x, k, tol, tol_mode,
+    return solve1d<float>(nx, ny, h, f, bc, x0, stencil, mode, tile_x, overlap_x, k, tol, tol_mode,
                           ref_residual, max_cycles, tile_order, x_out, hist, cycles, converged);
   }
   if (dim == 2) {
     if (mode == 0 && (tile_y < 1 || tile_y > ny)) return ST_INVALID;
     if (mode == 0 && (overlap_y < 0 || overlap_y % 2 != 0 || overlap_y >= tile_y)) return ST_INVALID;
     if (dtype == 0)
-      return solve2d<double>(nx, ny, h, f, bc, x0, mode, tile_x, tile_y, overlap_x, overlap_y, k,
-                             tol, tol_mode, ref_residual, max_cycles, tile_order, x_out, hist,
+      return solve2d<double>(nx, ny, h, f, bc, x0, stencil, mode, tile_x, tile_y, overlap_x, overlap_y,
+                             k, tol, tol_mode, ref_residual, max_cycles, tile_order, x_out, hist,
                              cycles, converged);
-    return solve2d<float>(nx, ny, h, f, bc, x0, mode, tile_x, tile_y, overlap_x, overlap_y, k, tol,
-                          tol_mode, ref_residual, max_cycles, tile_order, x_out, hist, cycles,
+    return solve2d<float>(nx, ny, h, f, bc, x0, stencil, mode, tile_x, tile_y, overlap_x, overlap_y, k,
+                          tol, tol_mode, ref_residual, max_cycles, tile_order, x_out, hist, cycles,
                           converged);
   }
   return ST_INVALID;
@@ -502,6 +596,46 @@ double hjo_residual(int dim, int64_t nx, int64_t ny, double h, const double* f, 
   for (int64_t j = 1; j <= ny; ++j)
     for (int64_t i = 1; i <= nx; ++i) xx[at(p, i, j)] = x[(j - 1) * nx + (i - 1)];
   return std::sqrt(residual_sq_2d(p, xx)) / h2;
+}
+
+// The general-coefficient residual by its plain definition (reading c23), in double from the
+// coefficients themselves (not the rounded weights): 2D ||b - Ax||_2 with
+// (Ax)_ij = a x_{i-1,j} + c x_{i+1,j} + e x_{i,j-1} + f x_{i,j+1} + d x_ij (Eq. 10's matrix);
+// 1D ||D^{-1}(b - Ax)||_2 with (Ax)_i = a_i x_{i-1} + d_i x_i + c_i x_{i+1} (Eq. 4's matrix),
+// over ny independent problems.  Ring values from bc as in hjo_solve.
+double hjo_residual_general(int dim, int64_t nx, int64_t ny, const double* f, const double* bc,
+                            const double* x, const double* stencil) {
+  double S = 0.0;
+  if (dim == 1) {
+    const int64_t nt = nx * ny;
+    for (int64_t b = 0; b < ny; ++b)
+      for (int64_t i = 0; i < nx; ++i) {
+        const int64_t g = b * nx + i;
+        const double xl = i > 0 ? x[g - 1] : (bc ? bc[2 * b] : 0.0);
+        const double xr = i < nx - 1 ? x[g + 1] : (bc ? bc[2 * b + 1] : 0.0);
+        const double ax = stencil[g] * xl + stencil[nt + g] * x[g] + stencil[2 * nt + g] * xr;
+        const double r = (f[g] - ax) / stencil[nt + g];
+        S += r * r;
+      }
+    return std::sqrt(S);
+  }
+  auto val = [&](int64_t i, int64_t j) -> double {  // 0-based interior, -1 / n = ring
+    if (i >= 0 && i < nx && j >= 0 && j < ny) return x[j * nx + i];
+    if (!bc) return 0.0;
+    if (j < 0) return bc[i];
+    if (j >= ny) return bc[nx + i];
+    if (i < 0) return bc[2 * nx + j];
+    return bc[2 * nx + ny + j];
+  };
+  for (int64_t j = 0; j < ny; ++j)
+    for (int64_t i = 0; i < nx; ++i) {
+      const double ax = stencil[0] * val(i - 1, j) + stencil[1] * val(i + 1, j) +
+                        stencil[2] * val(i, j - 1) + stencil[3] * val(i, j + 1) +
+                        stencil[4] * x[j * nx + i];
+      const double r = f[j * nx + i] - ax;
+      S += r * r;
+    }
+  return std::sqrt(S);
 }
 
 // Resource figures (o = 0):

@@ -13,6 +13,16 @@ and the CPU oracle consume.  Recipes:
   1D u = x^3 - x (f = -6x, g = 0); 2D u = x^2 + y^2 (f = -4, g = u on the
   ring, non-zero Dirichlet data).  x0 = 0.
 
+General coefficients (``make_general``; f is then b, h unused):
+
+* ``A`` — 2D anisotropic Poisson on the unit square with nx != ny: dx = 1/(nx+1), dy = 1/(ny+1),
+  {a, c, e, f, d} = {-1/dx^2, -1/dx^2, -1/dy^2, -1/dy^2, 2/dx^2 + 2/dy^2} (PAPER.md:413-419),
+  b = 1, x0 = 1, g = 0 (the paper's protocol on a rectangular grid).
+* ``G`` — random diagonally dominant coefficients with mixed signs (2D: five constants; 1D: a_i,
+  d_i, c_i per point), b, x0, g ~ U[-1, 1) (parity stress for every coefficient's position).
+* ``V`` — 1D variable-coefficient diffusion -(k u')' = 1, k(x) = 1 + 0.5 sin(2 pi x + 0.1 p) for
+  problem p: a_i = -k(x_i - h/2)/h^2, c_i = -k(x_i + h/2)/h^2, d_i = -(a_i + c_i); x0 = 1, g = 0.
+
 Grid: h = 1/(nx+1); interior node i (0-based) sits at x = (i+1) h; in 2D the
 same h is used along y (the ABI has one spacing, "if dx = dy").
 Arrays are row-major with x fastest: f[j*nx + i].  The 2D ring layout is
@@ -110,3 +120,52 @@ def exact_solution_Q(dim: int, nx: int, ny: int | None = None) -> np.ndarray:
     ny = nx if ny is None else ny
     ys = (np.arange(ny, dtype=np.float64) + 1.0) * h
     return (xs[None, :] ** 2 + ys[:, None] ** 2).reshape(-1)
+
+
+def make_general(recipe: str, dim: int, nx: int, ny: int | None = None, seed: int = SEED,
+                 batch: int = 1):
+    """General-coefficient problem: dict(dim, nx, ny, h, f (= b), bc, x0, stencil).
+
+    stencil: 2D {a, c, e, f, d} (west, east, south, north, centre; PAPER.md:344-347, Eq. 10);
+    1D the planes [a | d | c] of nx*batch values (Eq. 4; ny = batch)."""
+    if dim == 1:
+        ny = batch
+    elif ny is None:
+        ny = nx
+    n = nx * ny
+    nbc = 2 * ny if dim == 1 else 2 * nx + 2 * ny
+    if recipe == "A":
+        if dim != 2:
+            raise ValueError("recipe A is 2D")
+        dx, dy = 1.0 / (nx + 1), 1.0 / (ny + 1)
+        st = np.array([-1 / dx ** 2, -1 / dx ** 2, -1 / dy ** 2, -1 / dy ** 2, 2 / dx ** 2 + 2 / dy ** 2])
+        f, x0, bc = np.ones(n), np.ones(n), np.zeros(nbc)
+    elif recipe == "G":
+        u = (uniform_pm1(seed + 3 * n + 101, 3 * n + 8) + 1.0) / 2.0   # U[0, 1)
+        if dim == 2:
+            a, c, e, fn = -(0.2 + 0.8 * u[0]), -(0.2 + 0.8 * u[1]), 0.1 + 0.4 * u[2], -(0.2 + 0.8 * u[3])
+            d = (abs(a) + abs(c) + abs(e) + abs(fn)) * (1.02 + 0.3 * u[4])
+            st = np.array([a, c, e, fn, d])
+        else:
+            a = -(0.1 + 0.9 * u[:n])
+            c = u[n:2 * n] - 0.3
+            d = (np.abs(a) + np.abs(c)) * (1.02 + 0.5 * u[2 * n:3 * n])
+            st = np.concatenate([a, d, c])
+        f = uniform_pm1(seed, n)
+        x0 = uniform_pm1(seed + 7 * n + 13, n)
+        bc = uniform_pm1(seed + n, nbc)
+    elif recipe == "V":
+        if dim != 1:
+            raise ValueError("recipe V is 1D")
+        h = 1.0 / (nx + 1)
+        xs = (np.arange(nx, dtype=np.float64) + 1.0) * h
+        ph = 0.1 * np.arange(ny, dtype=np.float64)[:, None]
+        kl = 1.0 + 0.5 * np.sin(2 * np.pi * (xs[None, :] - h / 2) + ph)
+        kr = 1.0 + 0.5 * np.sin(2 * np.pi * (xs[None, :] + h / 2) + ph)
+        a, c = (-kl / h ** 2).reshape(-1), (-kr / h ** 2).reshape(-1)
+        st = np.concatenate([a, -(a + c), c])
+        f, x0, bc = np.ones(n), np.ones(n), np.zeros(nbc)
+    else:
+        raise ValueError(f"unknown recipe {recipe!r}")
+    return dict(dim=dim, nx=nx, ny=ny, h=1.0, f=np.ascontiguousarray(f), bc=bc,
+                x0=np.ascontiguousarray(x0), stencil=np.ascontiguousarray(st, dtype=np.float64))

@@ -159,3 +159,90 @@ def direct_solve(dim, nx, ny, h, f, bc=None):
             r[:, -1] += bc[2 * nx + ny:]
             rhs = r.reshape(-1)
     return spla.spsolve(A.tocsc(), rhs)
+
+
+def cycle_affine_general(dim, nx, ny, stencil, b, tx, ty, k, ox=0, oy=0):
+    """(M, g) of one hierarchical cycle for the general coefficients (Eq. 4 / Eq. 10) with EXACT
+    quotients: the Jacobi matrix of the tile is -D^-1 (offdiag) restricted to the tile, d_t = b/d."""
+    if dim == 1:
+        ny = 1
+    nz = (nx + 2) if dim == 1 else (nx + 2) * (ny + 2)
+    idx = ringed_index(nx, ny, dim)
+    b = np.asarray(b, dtype=np.float64).reshape(-1)
+    st = np.asarray(stencil, dtype=np.float64)
+
+    def coef(i, j):  # [(neighbour, coefficient)], diagonal
+        if dim == 1:
+            a, d, c = st[i - 1], st[nx + i - 1], st[2 * nx + i - 1]
+            return [((i - 1, 0), a), ((i + 1, 0), c)], d
+        a, c, e, f, d = st
+        return [((i - 1, j), a), ((i + 1, j), c), ((i, j - 1), e), ((i, j + 1), f)], d
+
+    interior = [(i, 0) for i in range(1, nx + 1)] if dim == 1 else \
+        [(i, j) for j in range(1, ny + 1) for i in range(1, nx + 1)]
+    out_pos = {p: q for q, p in enumerate(interior)}
+    M = np.zeros((len(interior), nz))
+    g = np.zeros(len(interior))
+    for T, owned in tiles(dim, nx, ny, tx, ty, ox, oy):
+        loc = {p: q for q, p in enumerate(T)}
+        w = len(T)
+        J, B, d_t, E = np.zeros((w, w)), np.zeros((w, nz)), np.zeros(w), np.zeros((w, nz))
+        for q, (i, j) in enumerate(T):
+            E[q, idx(i, j)] = 1.0
+            nb, dd = coef(i, j)
+            d_t[q] = b[out_pos[(i, j)]] / dd
+            for (ii, jj), cc in nb:
+                if (ii, jj) in loc:
+                    J[q, loc[(ii, jj)]] += -cc / dd
+                else:
+                    B[q, idx(ii, jj)] += -cc / dd
+        S = np.zeros((w, w))
+        Jp = np.eye(w)
+        for _ in range(k):
+            S += Jp
+            Jp = Jp @ J
+        Mt = Jp @ E + S @ B
+        gt = S @ d_t
+        for p in owned:
+            M[out_pos[p]] = Mt[loc[p]]
+            g[out_pos[p]] = gt[loc[p]]
+    return M, g
+
+
+def general_matrix(dim, nx, ny, stencil):
+    """Dense A of Eq. 4 (1D, one problem) / Eq. 10 (2D) on the interior unknowns."""
+    st = np.asarray(stencil, dtype=np.float64)
+    if dim == 1:
+        a, d, c = st[:nx], st[nx:2 * nx], st[2 * nx:]
+        return np.diag(d) + np.diag(a[1:], -1) + np.diag(c[:-1], 1)
+    a, c, e, f, d = st
+    n = nx * ny
+    A = np.zeros((n, n))
+    for j in range(ny):
+        for i in range(nx):
+            r = j * nx + i
+            A[r, r] = d
+            if i > 0: A[r, r - 1] = a
+            if i < nx - 1: A[r, r + 1] = c
+            if j > 0: A[r, r - nx] = e
+            if j < ny - 1: A[r, r + nx] = f
+    return A
+
+
+def general_rhs(dim, nx, ny, stencil, b, bc):
+    """b with the Dirichlet ring moved to the right-hand side."""
+    st = np.asarray(stencil, dtype=np.float64)
+    rhs = np.asarray(b, dtype=np.float64).reshape(-1).copy()
+    if bc is None:
+        return rhs
+    if dim == 1:
+        rhs[0] -= st[0] * bc[0]
+        rhs[-1] -= st[3 * nx - 1] * bc[1]
+        return rhs
+    a, c, e, f, d = st
+    r = rhs.reshape(ny, nx)
+    r[0, :] -= e * bc[:nx]
+    r[-1, :] -= f * bc[nx:2 * nx]
+    r[:, 0] -= a * bc[2 * nx:2 * nx + ny]
+    r[:, -1] -= c * bc[2 * nx + ny:]
+    return r.reshape(-1)
