@@ -11,6 +11,14 @@
  *                                                                      :382-387 (§4.1), App. A :532-575
  * until ||f - A x_c||_2 <= tol * ||f - A x_0||_2 (relative) or
  * ||f - A x_c||_2 <= tol (absolute).  Readings of the paper: DESIGN.md §3.
+ * With hj_problem.stencil set, the same methods solve the paper's general systems instead:
+ *   1D  tridiagonal A with per-point a_i, d_i, c_i, x_i <- (b_i - a_i x_{i-1} - c_i x_{i+1})/d_i
+ *                                                                      PAPER.md:69-83 (§3, Eq. 4)
+ *   2D  pentadiagonal A with constants a, c, e, f, d,
+ *       x_ij <- (b_ij - a x_{i-1,j} - c x_{i+1,j} - e x_{i,j-1} - f x_{i,j+1})/d
+ *                                                                      PAPER.md:329-347 (§4, Eq. 10)
+ *   (e.g. anisotropic Poisson, dx != dy: a = c = -1/dx^2, e = f = -1/dy^2, d = 2/dx^2 + 2/dy^2,
+ *   PAPER.md:413-419), evaluated as the FMA chain of DESIGN.md reading c23.
  *
  * Conventions shared by every entry point
  *  - Arrays are row-major with x fastest: f[j*nx + i], 0 <= i < nx, 0 <= j < ny.
@@ -70,10 +78,22 @@ typedef enum {
 typedef struct {
   int32_t dim;           /* 1 or 2                                                           */
   int64_t nx, ny;        /* interior points per direction; dim 1: ny = number of problems     */
-  double h;              /* grid spacing (hx == hy == h)                                      */
-  const double *f;       /* nx*ny right-hand side of -Δu = f (the paper's b)                  */
+  double h;              /* grid spacing (hx == hy == h); unused when stencil != NULL         */
+  const double *f;       /* nx*ny right-hand side of -Δu = f; with stencil: b of Ax = b       */
   const double *bc;      /* ring values (layout above) or NULL                               */
   const double *x0;      /* nx*ny initial guess or NULL                                       */
+  const double *stencil; /* NULL: the Poisson problem above.  Otherwise the general
+                            coefficients (reading c23), same memory space as f:
+                              dim 2: 5 doubles {a, c, e, f, d} = the coefficients of the west,
+                                     east, south, north neighbour and the point itself (Eq. 10);
+                              dim 1: 3*nx*ny doubles, planes [a | d | c] indexed like f (Eq. 4;
+                                     a of a problem's first point and c of its last multiply
+                                     the ring values).
+                            Every d must be non-zero and every value finite
+                            (HJ_ERR_INVALID_ARG).  The residual is then r = D^-1 (b - Ax) in the
+                            iterate's arithmetic; history/tolerances use ||r||*|d| in 2D
+                            (= ||b - Ax||) and ||r|| in 1D.  Jacobi converges for diagonally
+                            dominant A; divergence ends in HJ_ERR_NUMERIC or HJ_NOT_CONVERGED. */
 } hj_problem;
 
 typedef struct {

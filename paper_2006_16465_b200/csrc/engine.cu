@@ -82,6 +82,41 @@ __global__ void init_q_kernel(T* __restrict__ Q, long long fpitch, long long fro
   }
 }
 
+// General coefficients (reading c23): Q = T(b/d) with d a constant (2D, Eq. 10) or,
+// in 1D (Eq. 4), per point from the stencil planes [a | d | c] together with WL = T(-a_i/d_i)
+// and WR = T(-c_i/d_i).  Padding entries are 0.
+template <typename T>
+__global__ void init_gen_kernel(T* __restrict__ Q, T* __restrict__ WL, T* __restrict__ WR,
+                                long long fpitch, long long frows, long long nx, long long ny,
+                                const double* __restrict__ f, const double* __restrict__ st,
+                                double d2) {
+  const long long n = fpitch * frows, nt = nx * ny;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long j = q / fpitch, i = q % fpitch;
+    const bool in = i < nx && j < ny;
+    const long long g = j * nx + i;
+    if (WL) {
+      const double d = in ? st[nt + g] : 1.0;
+      Q[q] = in ? (T)(f[g] / d) : T(0);
+      WL[q] = in ? (T)(-st[g] / d) : T(0);
+      WR[q] = in ? (T)(-st[2 * nt + g] / d) : T(0);
+    } else {
+      Q[q] = in ? (T)(f[g] / d2) : T(0);
+    }
+  }
+}
+
+// Count of invalid coefficients: non-finite anywhere, or a zero diagonal (1D: plane d).
+__global__ void check_stencil_kernel(const double* __restrict__ st, long long n, long long d_lo,
+                                     long long d_hi, unsigned long long* __restrict__ bad) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const double v = st[q];
+    if (!isfinite(v) || (q >= d_lo && q < d_hi && v == 0.0)) atomicAdd(bad, 1ULL);
+  }
+}
+
 // Extract the interior of X into a dense double array (row-major).
 template <typename T>
 __global__ void extract_kernel(const T* __restrict__ X, long long pitch, int dim, long long nx,
@@ -110,6 +145,7 @@ __global__ void rowsum_kernel(const double* __restrict__ part, long long ppr, lo
 // S_c = sum of R (fixed order); history; the stopping test of DESIGN.md §3 (c1, c14):
 // c = 0: converged iff S_0 == 0 (or the test holds with an explicit r_0 / absolute mode);
 // c >= 1: converged iff sqrt(S_c) <= tol * sqrt(S_0)  (absolute: sqrt(S_c)/h^2 <= tol).
+// h2 here is Geom::rdiv (h^2 for the Poisson problem; DESIGN.md c3, c23).
 __global__ void finalize_kernel(const double* __restrict__ R, long long nrg, Ctrl* __restrict__ ctrl,
                                 double* __restrict__ hist, long long hist_cap, double h2, double tol,
                                 int tol_mode, double ref_residual, long long max_cycles) {
@@ -227,7 +263,7 @@ hj_status validate(const hj_problem* pb, const hj_params* pr, bool need_f) {
     set_error("nx, ny must be >= 1");
     return HJ_ERR_INVALID_ARG;
   }
-  if (!(pb->h > 0.0) || !std::isfinite(pb->h)) { set_error("h must be finite and > 0"); return HJ_ERR_INVALID_ARG; }
+  if (!pb->stencil && (!(pb->h > 0.0) || !std::isfinite(pb->h))) { set_error("h must be finite and > 0"); return HJ_ERR_INVALID_ARG; }
   if (need_f && !pb->f) { set_error("f is NULL"); return HJ_ERR_INVALID_ARG; }
   if (pb->nx > (1LL << 30) || pb->ny > (1LL << 30)) { set_error("grid too large"); return HJ_ERR_INVALID_ARG; }
   if (pr->mode != HJ_HIERARCHICAL && pr->mode != HJ_CLASSIC) { set_error("bad mode"); return HJ_ERR_INVALID_CONFIG; }
@@ -280,7 +316,8 @@ static hj_status choose_kernel(const hj_problem* pb, const hj_params* pr, int* k
     return HJ_OK;
   }
   const int t = pr->tile_x;
-  if (pr->kernel == HJ_KERNEL_AUTO && pr->overlap == 0 && t % 32 == 0 && t <= 1024 &&
+  // general coefficients keep x, q, wL, wR of a lane in registers: tiles up to 256 points
+  if (pr->kernel == HJ_KERNEL_AUTO && pr->overlap == 0 && t % 32 == 0 && t <= (pb->stencil ? 256 : 1024) &&
       ((t / 32) & (t / 32 - 1)) == 0) {
     *kind = K_REG1D;
     return HJ_OK;
@@ -304,6 +341,8 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
   g.mode = pr->mode;
   g.h = pb->h;
   g.h2 = pb->h * pb->h;
+  g.gen = pb->stencil != nullptr;
+  g.rdiv = g.h2;
   g.nx = pb->nx;
   const long long ny_global = pb->ny;
   g.ny = di ? (di->row_end - di->row_begin) : pb->ny;
@@ -394,6 +433,10 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
   PCK(cudaMalloc(&P->X[0], xbytes));
   PCK(cudaMalloc(&P->X[1], xbytes));
   PCK(cudaMalloc(&P->H2F, fbytes));
+  if (g.gen && g.dim == 1) {
+    PCK(cudaMalloc(&P->WL, fbytes));
+    PCK(cudaMalloc(&P->WR, fbytes));
+  }
   PCK(cudaMalloc(&P->part, sizeof(double) * (g.nparts + 1)));
   PCK(cudaMalloc(&P->rowpart, sizeof(double) * (g.nrg_global + 1)));
   P->rowsum_dst = P->rowpart;
@@ -420,7 +463,52 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
   else PCK(cudaMemsetAsync(P->x0_d, 0, sizeof(double) * nloc, st));
   PCK(cudaMemsetAsync(P->rowpart, 0, sizeof(double) * (g.nrg_global + 1), st));
   PCK(cudaMemsetAsync(P->part, 0, sizeof(double) * (g.nparts + 1), st));
-  {
+  if (g.gen) {
+    // general coefficients (c23): device copy of the stencil (host or device pointer), checked on
+    // the device (finite, non-zero diagonal), then Q / weights
+    const long long ns = g.dim == 1 ? 3 * nloc : 5;
+    double* st_d = nullptr;
+    unsigned long long* bad_d = nullptr;
+    unsigned long long bad = 0;
+    double st5[5] = {0, 0, 0, 0, 1};
+    PCK(cudaMalloc(&st_d, sizeof(double) * ns + sizeof(unsigned long long)));
+    bad_d = reinterpret_cast<unsigned long long*>(st_d + ns);
+    cudaError_t e = cudaMemcpyAsync(st_d, pb->stencil, sizeof(double) * ns, cudaMemcpyDefault, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(bad_d, 0, sizeof(unsigned long long), st);
+    if (e == cudaSuccess) {
+      check_stencil_kernel<<<4 * nsm, 256, 0, st>>>(st_d, ns, g.dim == 1 ? nloc : 4, g.dim == 1 ? 2 * nloc : 5, bad_d);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, bad_d, sizeof(bad), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && g.dim == 2) e = cudaMemcpyAsync(st5, st_d, sizeof(st5), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess && bad == 0) {
+      if (g.dim == 2) {
+        for (int q = 0; q < 4; ++q)  // T-rounded weights, exact in double
+          g.wt[q] = esz == 8 ? -st5[q] / st5[4] : (double)(float)(-st5[q] / st5[4]);
+        g.rdiv = 1.0 / std::fabs(st5[4]);
+      } else {
+        g.rdiv = 1.0;
+      }
+      if (esz == 8)
+        init_gen_kernel<double><<<4 * nsm, 256, 0, st>>>((double*)P->H2F, (double*)P->WL, (double*)P->WR,
+                                                         g.fpitch, g.frows, g.nx, g.ny, pb->f, st_d, st5[4]);
+      else
+        init_gen_kernel<float><<<4 * nsm, 256, 0, st>>>((float*)P->H2F, (float*)P->WL, (float*)P->WR,
+                                                        g.fpitch, g.frows, g.nx, g.ny, pb->f, st_d, st5[4]);
+      e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    }
+    cudaFree(st_d);
+    if (e != cudaSuccess) {
+      set_error(std::string("stencil setup: ") + cudaGetErrorString(e));
+      return fail(HJ_ERR_CUDA);
+    }
+    if (bad) {
+      set_error("stencil: non-finite coefficient or zero diagonal");
+      return fail(HJ_ERR_INVALID_ARG);
+    }
+  } else {
     const int blocks = 4 * nsm;
     const double scale = g.dim == 2 ? 0.25 : 0.5;
     if (esz == 8)
@@ -491,6 +579,8 @@ hj_status launch_cycle(hj_plan* P, int p, bool timed, float* acc_ms) {
   a.xin = P->X[p];
   a.xout = P->X[p ^ 1];
   a.h2f = P->H2F;
+  a.wl = P->WL;
+  a.wr = P->WR;
   a.tm_in = &P->tmX[p];
   a.tm_f = &P->tmF;
   a.tm_out = &P->tmXs[p ^ 1];
@@ -522,7 +612,7 @@ hj_status launch_cycle(hj_plan* P, int p, bool timed, float* acc_ms) {
       P->part, g.parts_per_row, g.nrg_local, g.rg_offset, P->rowsum_dst, P->ctrl);
   HJ_CUDA(cudaGetLastError());
   if (P->dist) HJ_TRY(dist_allreduce(P));
-  finalize_kernel<<<1, 1024, 0, st>>>(P->rowpart, g.nrg_global, P->ctrl, P->hist, P->hist_cap, g.h2,
+  finalize_kernel<<<1, 1024, 0, st>>>(P->rowpart, g.nrg_global, P->ctrl, P->hist, P->hist_cap, g.rdiv,
                                       P->prm.tol, (int)P->prm.tol_mode, P->prm.ref_residual,
                                       P->prm.max_cycles);
   HJ_CUDA(cudaGetLastError());
@@ -633,8 +723,8 @@ hj_status plan_solve(hj_plan* P, hj_result* res, double* x_dev, double* hist_dev
   HJ_CUDA(cudaStreamSynchronize(st));
   res->cycles = cd;
   res->converged = c.converged;
-  res->initial_residual = std::sqrt(c.S0) / g.h2;
-  res->final_residual = std::sqrt(c.S_last) / g.h2;
+  res->initial_residual = std::sqrt(c.S0) / g.rdiv;
+  res->final_residual = std::sqrt(c.S_last) / g.rdiv;
   res->seconds_solve = ms * 1e-3;
   // the plan is now "used": reset before another solve
   return (hj_status)c.status;
@@ -647,6 +737,8 @@ void plan_free(hj_plan* P) {
   cudaFree(P->X[0]);
   cudaFree(P->X[1]);
   cudaFree(P->H2F);
+  cudaFree(P->WL);
+  cudaFree(P->WR);
   cudaFree(P->part);
   cudaFree(P->rowpart);
   cudaFree(P->rowpart_local);

@@ -76,6 +76,9 @@ __host__ __device__ __forceinline__ int axis_own_lo(const Axis& a, int b) {
 //   16-byte boundary so that pairs of doubles are one 128-bit access.
 struct Geom {
   int dim, dtype, mode, kernel_kind;
+  int gen;                     // general coefficients (hj_problem.stencil, DESIGN.md c23)
+  double wt[4];                // 2D general: T(-a/d), T(-c/d), T(-e/d), T(-f/d), exact in double
+  double rdiv;                 // reported residual = sqrt(S) / rdiv: h^2, 1/|d| (2D general), 1
   int64_t nx, ny;            // local interior extent (dist: the slab's rows)
   int64_t pitch, col0, rows; // X layout (elements)
   int64_t fpitch, frows;     // H2F layout: H2F[j*fpitch + i]
@@ -95,7 +98,10 @@ enum KernelKind { K_REG2D = 0, K_SMEM2D = 1, K_CLASSIC2D = 2, K_REG1D = 3, K_SME
 struct CycleArgs {
   const void* xin;
   void* xout;
-  const void* h2f;             // Q = T(h^2 f) / diag (0.25 in 2D, 0.5 in 1D), see init_q_kernel
+  const void* h2f;             // Q = T(h^2 f) / diag (0.25 in 2D, 0.5 in 1D), see init_q_kernel;
+                               // general coefficients: Q = T(b / d)
+  const void* wl;              // 1D general: T(-a_i/d_i), same layout as Q (else NULL)
+  const void* wr;              // 1D general: T(-c_i/d_i)
   const CUtensorMap* tm_in;   // TMA descriptor of xin, 34 x (col0+34) box (REG2D loads)
   const CUtensorMap* tm_f;    // TMA descriptor of h2f, 32 x 32 box (REG2D loads)
   const CUtensorMap* tm_out;  // TMA descriptor of xout, 32 x 32 box (REG2D stores)
@@ -207,6 +213,35 @@ __device__ __forceinline__ double res2(double x, double w, double e, double s, d
 }
 __device__ __forceinline__ double res1(double x, double l, double r, double h2f) {
   return h2f - (2.0 * x - (l + r));
+}
+
+// General coefficients (PAPER.md:80-83 Eq. 4, :344-347 Eq. 10; reading c23): the
+// division distributed over the terms, weights w = T(-coef/d), q = T(b/d):
+//   2D: fma(wN, N, fma(wS, S, fma(wE, E, fma(wW, W, q))))      1D: fma(wR, R, fma(wL, L, q))
+// and the Jacobi-scaled residual D^{-1}(b - Ax) = (the same chain in double) - x.
+struct Wt2 {
+  double w, e, s, n;
+};
+__device__ __forceinline__ double gupd2(double ww, double we, double ws, double wn, double W,
+                                        double E, double S, double N, double q) {
+  return __fma_rn(wn, N, __fma_rn(ws, S, __fma_rn(we, E, __fma_rn(ww, W, q))));
+}
+__device__ __forceinline__ float gupd2(float ww, float we, float ws, float wn, float W, float E,
+                                       float S, float N, float q) {
+  return __fmaf_rn(wn, N, __fmaf_rn(ws, S, __fmaf_rn(we, E, __fmaf_rn(ww, W, q))));
+}
+__device__ __forceinline__ double gres2(double ww, double we, double ws, double wn, double x,
+                                        double W, double E, double S, double N, double q) {
+  return __dsub_rn(gupd2(ww, we, ws, wn, W, E, S, N, q), x);
+}
+__device__ __forceinline__ double gupd1(double wl, double wr, double L, double R, double q) {
+  return __fma_rn(wr, R, __fma_rn(wl, L, q));
+}
+__device__ __forceinline__ float gupd1(float wl, float wr, float L, float R, float q) {
+  return __fmaf_rn(wr, R, __fmaf_rn(wl, L, q));
+}
+__device__ __forceinline__ double gres1(double wl, double wr, double x, double L, double R, double q) {
+  return __dsub_rn(gupd1(wl, wr, L, R, q), x);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {

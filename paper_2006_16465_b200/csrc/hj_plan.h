@@ -30,6 +30,8 @@ struct hj_plan {
   long long ny_global = 0, gy0 = 0;
   void* X[2] = {nullptr, nullptr};
   void* H2F = nullptr;
+  void* WL = nullptr;               // 1D general coefficients: T(-a_i/d_i), layout of H2F
+  void* WR = nullptr;               //                          T(-c_i/d_i)
   double* part = nullptr;
   double* rowpart = nullptr;        // per row group sums, global length (input of finalize)
   double* rowpart_local = nullptr;  // dist: this rank's row groups, zeros elsewhere

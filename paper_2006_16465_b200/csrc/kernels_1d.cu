@@ -4,6 +4,9 @@
 // point left and right to on-chip memory, performs k sub-iterations of the update
 // x_i <- (b_i dx^2 + x_{i-1} + x_{i+1})/2 with the two halo points frozen, and
 // writes the interior back.  Residual of the snapshot fused: s = h2f - (2x - (L+R)).
+// GEN = true: the general tridiagonal update of Eq. 4 with per-point weights
+// wL = T(-a_i/d_i), wR = T(-c_i/d_i) stored like Q (= T(b_i/d_i)); update / residual gupd1 / gres1
+// (reading c23).
 #include "hj_internal.cuh"
 
 namespace hj {
@@ -17,7 +20,7 @@ constexpr unsigned FULL = 0xffffffffu;
 // neighbours across lanes by one shuffle each way per sub-iteration; tile + halo staged in
 // shared memory by the TMA bulk-copy engine (cp.async.bulk), double-buffered per warp.
 // =============================================================================
-template <typename T, int C>
+template <typename T, int C, bool GEN = false>
 struct R1 {
   static constexpr int TILE = 32 * C;
   static constexpr int COL0 = 16 / sizeof(T);
@@ -25,23 +28,37 @@ struct R1 {
   static constexpr int XBYTES = XN * sizeof(T);
   static constexpr int XSLOT = (XBYTES + 127) / 128 * 128;
   static constexpr int FBYTES = TILE * sizeof(T);
-  static constexpr int SLOT = XSLOT + (FBYTES + 127) / 128 * 128;
+  static constexpr int FSLOT = (FBYTES + 127) / 128 * 128;
+  static constexpr int NF = GEN ? 3 : 1;                      // q (+ wL, wR)
+  static constexpr int SLOT = XSLOT + NF * FSLOT;
   static constexpr int WARPS = 4;
   static constexpr size_t SMEM = 128 + 128 + size_t(WARPS) * 2 * SLOT;
+  static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <typename T, int C, bool RAGGED>
-__device__ __forceinline__ void reg1d_tile(const T* __restrict__ sx, const T* __restrict__ sf,
+// Source pointers of one tile: x (with halo), q and, for GEN, the weight arrays.
+template <typename T>
+struct Src1 {
+  const T *x, *q, *wl, *wr;
+};
+
+template <typename T, int C, bool RAGGED, bool GEN>
+__device__ __forceinline__ void reg1d_tile(const unsigned char* __restrict__ sl,
                                            T* __restrict__ xrow, long long t, int w, int lane,
                                            int kk, double* __restrict__ part, long long u,
-                                           uint64_t* bar, const T* nx_src, const T* nq_src,
-                                           void* slot_x, void* slot_f) {
-  using P = R1<T, C>;
-  T x[C], q[C];
+                                           uint64_t* bar, const Src1<T>* nxt, unsigned char* slot) {
+  using P = R1<T, C, GEN>;
+  const T* sx = reinterpret_cast<const T*>(sl);
+  const T* sf = reinterpret_cast<const T*>(sl + P::XSLOT);
+  T x[C], q[C], wl[GEN ? C : 1], wr[GEN ? C : 1];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     x[c] = sx[P::COL0 + C * lane + c];
     q[c] = sf[C * lane + c];
+    if constexpr (GEN) {
+      wl[c] = sf[P::FSLOT / sizeof(T) + C * lane + c];
+      wr[c] = sf[2 * P::FSLOT / sizeof(T) + C * lane + c];
+    }
   }
   const T hl = sx[P::COL0 - 1];       // frozen left halo (used by lane 0)
   const T hr = sx[P::COL0 + P::TILE]; // frozen right halo (used by lane 31) — for a ragged
@@ -64,18 +81,24 @@ __device__ __forceinline__ void reg1d_tile(const T* __restrict__ sx, const T* __
     for (int c = 0; c < C; ++c) {
       const T L = c == 0 ? l : x[c - 1];
       const T R = c == C - 1 ? r : x[c + 1];
-      const double s = res1((double)x[c], (double)L, (double)R, (double)(T(2) * q[c]));
+      double s;
+      if constexpr (GEN) s = gres1((double)wl[c], (double)wr[c], (double)x[c], (double)L, (double)R, (double)q[c]);
+      else s = res1((double)x[c], (double)L, (double)R, (double)(T(2) * q[c]));
       if ((act >> c) & 1u) acc = __fma_rn(s, s, acc);
     }
   }
   acc = warp_sum(acc);
   if (lane == 0) part[u] = acc;
   __syncwarp();
-  if (lane == 0 && nx_src) {  // the slot is free: prefetch this warp's next tile into it
+  if (lane == 0 && nxt) {  // the slot is free: prefetch this warp's next tile into it
     fence_proxy_async();
-    mbar_arrive_expect_tx(bar, P::XBYTES + P::FBYTES);
-    bulk_load(slot_x, nx_src, P::XBYTES, bar);
-    bulk_load(slot_f, nq_src, P::FBYTES, bar);
+    mbar_arrive_expect_tx(bar, P::XBYTES + P::NF * P::FBYTES);
+    bulk_load(slot, nxt->x, P::XBYTES, bar);
+    bulk_load(slot + P::XSLOT, nxt->q, P::FBYTES, bar);
+    if constexpr (GEN) {
+      bulk_load(slot + P::XSLOT + P::FSLOT, nxt->wl, P::FBYTES, bar);
+      bulk_load(slot + P::XSLOT + 2 * P::FSLOT, nxt->wr, P::FBYTES, bar);
+    }
   }
 #pragma unroll 1
   for (int s = 0; s < kk; ++s) {
@@ -87,7 +110,9 @@ __device__ __forceinline__ void reg1d_tile(const T* __restrict__ sx, const T* __
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       const T R = c == C - 1 ? r : x[c + 1];
-      const T nv = upd1(prev, R, q[c]);
+      T nv;
+      if constexpr (GEN) nv = gupd1(wl[c], wr[c], prev, R, q[c]);
+      else nv = upd1(prev, R, q[c]);
       prev = x[c];
       if (!RAGGED || ((act >> c) & 1u)) x[c] = nv;
     }
@@ -100,12 +125,13 @@ __device__ __forceinline__ void reg1d_tile(const T* __restrict__ sx, const T* __
 
 // Rows of the padded arrays are independent problems (batched 1D); tile u of the
 // launch is tile (u % ntpr) of problem (u / ntpr), and its residual partial is part[u].
-template <typename T, int C>
-__global__ void __launch_bounds__(R1<T, C>::WARPS * 32)
-reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restrict__ h2f, int nx,
-             long long pitch, long long fpitch, int ntpr, long long ntiles,
-             double* __restrict__ part, const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
-  using P = R1<T, C>;
+template <typename T, int C, bool GEN>
+__global__ void __launch_bounds__(R1<T, C, GEN>::WARPS * 32)
+reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restrict__ h2f,
+             const T* __restrict__ wla, const T* __restrict__ wra, int nx, long long pitch,
+             long long fpitch, int ntpr, long long ntiles, double* __restrict__ part,
+             const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
+  using P = R1<T, C, GEN>;
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
   extern __shared__ unsigned char smem_raw[];
@@ -118,8 +144,11 @@ reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restric
   const long long gw = (long long)blockIdx.x * P::WARPS + warp;
   const long long nw = (long long)gridDim.x * P::WARPS;
   if (gw >= ntiles) return;
-  auto src_x = [&](long long u) { return xin + (u / ntpr) * pitch + (u % ntpr) * P::TILE; };
-  auto src_q = [&](long long u) { return h2f + (u / ntpr) * fpitch + (u % ntpr) * P::TILE; };
+  auto src = [&](long long u) {
+    const long long fo = (u / ntpr) * fpitch + (u % ntpr) * P::TILE;
+    return Src1<T>{xin + (u / ntpr) * pitch + (u % ntpr) * P::TILE, h2f + fo,
+                   GEN ? wla + fo : nullptr, GEN ? wra + fo : nullptr};
+  };
   if (lane == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -128,9 +157,14 @@ reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restric
       const long long u = gw + s * nw;
       if (u < ntiles) {
         unsigned char* sl = s ? slot1 : slot0;
-        mbar_arrive_expect_tx(&bars[s], P::XBYTES + P::FBYTES);
-        bulk_load(sl, src_x(u), P::XBYTES, &bars[s]);
-        bulk_load(sl + P::XSLOT, src_q(u), P::FBYTES, &bars[s]);
+        const Src1<T> sr = src(u);
+        mbar_arrive_expect_tx(&bars[s], P::XBYTES + P::NF * P::FBYTES);
+        bulk_load(sl, sr.x, P::XBYTES, &bars[s]);
+        bulk_load(sl + P::XSLOT, sr.q, P::FBYTES, &bars[s]);
+        if constexpr (GEN) {
+          bulk_load(sl + P::XSLOT + P::FSLOT, sr.wl, P::FBYTES, &bars[s]);
+          bulk_load(sl + P::XSLOT + 2 * P::FSLOT, sr.wr, P::FBYTES, &bars[s]);
+        }
       }
     }
   }
@@ -143,15 +177,13 @@ reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restric
     const long long t = u % ntpr;
     const int w = (int)lmin(P::TILE, nx - t * P::TILE);
     const long long un = u + 2 * nw;
-    const T* nxs = un < ntiles ? src_x(un) : nullptr;
-    const T* nqs = un < ntiles ? src_q(un) : nullptr;
-    const T* sx = reinterpret_cast<const T*>(sl);
-    const T* sf = reinterpret_cast<const T*>(sl + P::XSLOT);
+    const Src1<T> nsr = un < ntiles ? src(un) : Src1<T>{nullptr, nullptr, nullptr, nullptr};
+    const Src1<T>* nxt = un < ntiles ? &nsr : nullptr;
     T* xrow = xout + (u / ntpr) * pitch;
     if (w == P::TILE)
-      reg1d_tile<T, C, false>(sx, sf, xrow, t, w, lane, kk, part, u, &bars[s], nxs, nqs, sl, sl + P::XSLOT);
+      reg1d_tile<T, C, false, GEN>(sl, xrow, t, w, lane, kk, part, u, &bars[s], nxt, sl);
     else
-      reg1d_tile<T, C, true>(sx, sf, xrow, t, w, lane, kk, part, u, &bars[s], nxs, nqs, sl, sl + P::XSLOT);
+      reg1d_tile<T, C, true, GEN>(sl, xrow, t, w, lane, kk, part, u, &bars[s], nxt, sl);
   }
 }
 
@@ -161,9 +193,10 @@ reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restric
 // sub-iteration, write-back of the latest container (reading c8), into the other global
 // buffer (reading c6), rhs of the updated point (reading c7).
 // =============================================================================
-template <typename T>
+template <typename T, bool GEN>
 __global__ void smem1d_kernel(const T* __restrict__ xin_all, T* __restrict__ xout_all,
-                              const T* __restrict__ h2f_all, int nx, long long pitch,
+                              const T* __restrict__ h2f_all, const T* __restrict__ wla,
+                              const T* __restrict__ wra, int nx, long long pitch,
                               long long fpitch, Axis ax, double* __restrict__ part,
                               const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
   // block = (problem row, subdomain): rows of the padded arrays are independent problems
@@ -194,10 +227,17 @@ __global__ void smem1d_kernel(const T* __restrict__ xin_all, T* __restrict__ xou
   const bool active = a < w;
   const bool owned = a >= o0 && a <= o1;   // overlapping blocks write only what they own
   if (active) rhs[a] = h2f[i0 + a];
+  T wl = T(0), wr = T(0);   // GEN: this point's weights (registers; the paper keeps b only)
+  if (GEN && active) {
+    wl = wla[row * fpitch + i0 + a];
+    wr = wra[row * fpitch + i0 + a];
+  }
   __syncthreads();
   double s2 = 0.0;
   if (owned) {
-    const double s = res1((double)A[a + 1], (double)A[a], (double)A[a + 2], (double)(T(2) * rhs[a]));
+    const double s =
+        GEN ? gres1((double)wl, (double)wr, (double)A[a + 1], (double)A[a], (double)A[a + 2], (double)rhs[a])
+            : res1((double)A[a + 1], (double)A[a], (double)A[a + 2], (double)(T(2) * rhs[a]));
     s2 = s * s;
   }
   s2 = warp_sum(s2);
@@ -212,7 +252,7 @@ __global__ void smem1d_kernel(const T* __restrict__ xin_all, T* __restrict__ xou
   T* cur = A;
   T* nxt = B;
   for (int s = 0; s < kk; ++s) {
-    if (active) nxt[a + 1] = upd1(cur[a], cur[a + 2], q2);
+    if (active) nxt[a + 1] = GEN ? gupd1(wl, wr, cur[a], cur[a + 2], q2) : upd1(cur[a], cur[a + 2], q2);
     __syncthreads();
     T* tmp = cur; cur = nxt; nxt = tmp;
   }
@@ -223,10 +263,11 @@ __global__ void smem1d_kernel(const T* __restrict__ xin_all, T* __restrict__ xou
 // CLASSIC1D — one sweep; 256 threads x 8 consecutive points per CTA (128-bit loads),
 // neighbours by shuffle, fused residual, one partial per CTA.
 // =============================================================================
-template <typename T>
+template <typename T, bool GEN>
 __global__ void __launch_bounds__(256)
 classic1d_kernel(const T* __restrict__ xin_all, T* __restrict__ xout_all,
-                 const T* __restrict__ h2f_all, int nx, long long pitch, long long fpitch, int ncb,
+                 const T* __restrict__ h2f_all, const T* __restrict__ wla, const T* __restrict__ wra,
+                 int nx, long long pitch, long long fpitch, int ncb,
                  double* __restrict__ part, const Ctrl* __restrict__ ctrl, long long max_cycles) {
   const long long row = blockIdx.x / ncb;  // independent problem
   const T* __restrict__ xin = xin_all + row * pitch;
@@ -257,9 +298,16 @@ classic1d_kernel(const T* __restrict__ xin_all, T* __restrict__ xout_all,
     const T L = c == 0 ? l : x[c - 1];
     const T R = c == V - 1 ? r : x[c + 1];
     if (i < nx) {
-      const double s = res1((double)x[c], (double)L, (double)R, (double)(T(2) * f[c]));
-      acc = __fma_rn(s, s, acc);
-      if (write) xout[COL0 + i] = upd1(L, R, f[c]);
+      if constexpr (GEN) {
+        const T wl = wla[row * fpitch + i], wr = wra[row * fpitch + i];
+        const double s = gres1((double)wl, (double)wr, (double)x[c], (double)L, (double)R, (double)f[c]);
+        acc = __fma_rn(s, s, acc);
+        if (write) xout[COL0 + i] = gupd1(wl, wr, L, R, f[c]);
+      } else {
+        const double s = res1((double)x[c], (double)L, (double)R, (double)(T(2) * f[c]));
+        acc = __fma_rn(s, s, acc);
+        if (write) xout[COL0 + i] = upd1(L, R, f[c]);
+      }
     }
   }
   acc = warp_sum(acc);
@@ -272,45 +320,45 @@ classic1d_kernel(const T* __restrict__ xin_all, T* __restrict__ xout_all,
   }
 }
 
-template <typename T, int C>
+template <typename T, int C, bool GEN>
 void launch_reg1d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
-  using P = R1<T, C>;
+  using P = R1<T, C, GEN>;
   long long ctas = (g.ntiles + P::WARPS - 1) / P::WARPS;
   if (ctas > grid_hint) ctas = grid_hint;
-  reg1d_kernel<T, C><<<(unsigned)ctas, P::WARPS * 32, P::SMEM, st>>>(
-      (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (int)g.nx, g.pitch, g.fpitch, (int)g.ntx,
-      g.ntiles, a.part, a.ctrl, g.k, a.max_cycles);
+  reg1d_kernel<T, C, GEN><<<(unsigned)ctas, P::WARPS * 32, P::SMEM, st>>>(
+      (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (const T*)a.wl, (const T*)a.wr, (int)g.nx,
+      g.pitch, g.fpitch, (int)g.ntx, g.ntiles, a.part, a.ctrl, g.k, a.max_cycles);
 }
 
-template <typename T>
+template <typename T, bool GEN>
 cudaError_t launch_1d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
   if (g.kernel_kind == K_REG1D) {
-    switch (g.tx / 32) {
-      case 1: launch_reg1d<T, 1>(g, a, grid_hint * 8, st); break;
-      case 2: launch_reg1d<T, 2>(g, a, grid_hint * 8, st); break;
-      case 4: launch_reg1d<T, 4>(g, a, grid_hint * 4, st); break;
-      case 8: launch_reg1d<T, 8>(g, a, grid_hint * 4, st); break;
-      case 16: launch_reg1d<T, 16>(g, a, grid_hint * 2, st); break;
-      case 32: launch_reg1d<T, 32>(g, a, grid_hint, st); break;
+    switch (g.tx / 32) {   // GEN: tiles <= 256 (x, q, wL, wR of a lane in registers)
+      case 1: launch_reg1d<T, 1, GEN>(g, a, grid_hint * 8, st); break;
+      case 2: launch_reg1d<T, 2, GEN>(g, a, grid_hint * 8, st); break;
+      case 4: launch_reg1d<T, 4, GEN>(g, a, grid_hint * 4, st); break;
+      case 8: launch_reg1d<T, 8, GEN>(g, a, grid_hint * 4, st); break;
+      case 16: if (GEN) return cudaErrorInvalidValue; launch_reg1d<T, 16, false>(g, a, grid_hint * 2, st); break;
+      case 32: if (GEN) return cudaErrorInvalidValue; launch_reg1d<T, 32, false>(g, a, grid_hint, st); break;
       default: return cudaErrorInvalidValue;
     }
   } else if (g.kernel_kind == K_SMEM1D) {
     const size_t smem = sizeof(T) * (2 * size_t(g.tx + 2) + size_t(g.tx));
-    smem1d_kernel<T><<<(unsigned)g.ntiles, g.tx, smem, st>>>(
-        (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (int)g.nx, g.pitch, g.fpitch, g.ax, a.part,
-        a.ctrl, g.k, a.max_cycles);
+    smem1d_kernel<T, GEN><<<(unsigned)g.ntiles, g.tx, smem, st>>>(
+        (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (const T*)a.wl, (const T*)a.wr, (int)g.nx,
+        g.pitch, g.fpitch, g.ax, a.part, a.ctrl, g.k, a.max_cycles);
   } else {
-    classic1d_kernel<T><<<(unsigned)g.ntiles, 256, 0, st>>>(
-        (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (int)g.nx, g.pitch, g.fpitch, (int)g.ntx, a.part,
-        a.ctrl, a.max_cycles);
+    classic1d_kernel<T, GEN><<<(unsigned)g.ntiles, 256, 0, st>>>(
+        (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (const T*)a.wl, (const T*)a.wr, (int)g.nx,
+        g.pitch, g.fpitch, (int)g.ntx, a.part, a.ctrl, a.max_cycles);
   }
   return cudaGetLastError();
 }
 
-template <typename T, int C>
+template <typename T, int C, bool GEN = false>
 cudaError_t cfg1() {
-  return cudaFuncSetAttribute(reg1d_kernel<T, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)R1<T, C>::SMEM);
+  return cudaFuncSetAttribute(reg1d_kernel<T, C, GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)R1<T, C, GEN>::SMEM);
 }
 
 }  // namespace
@@ -326,7 +374,9 @@ cudaError_t configure_1d() {
 #define HJ_CFG(T)                                                                              \
   if ((e = cfg1<T, 1>()) != cudaSuccess || (e = cfg1<T, 2>()) != cudaSuccess ||                \
       (e = cfg1<T, 4>()) != cudaSuccess || (e = cfg1<T, 8>()) != cudaSuccess ||                \
-      (e = cfg1<T, 16>()) != cudaSuccess || (e = cfg1<T, 32>()) != cudaSuccess)                \
+      (e = cfg1<T, 16>()) != cudaSuccess || (e = cfg1<T, 32>()) != cudaSuccess ||              \
+      (e = cfg1<T, 1, true>()) != cudaSuccess || (e = cfg1<T, 2, true>()) != cudaSuccess ||    \
+      (e = cfg1<T, 4, true>()) != cudaSuccess || (e = cfg1<T, 8, true>()) != cudaSuccess)      \
     return e;
   HJ_CFG(double)
   HJ_CFG(float)
@@ -335,8 +385,11 @@ cudaError_t configure_1d() {
 }
 
 cudaError_t launch_cycle_1d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
-  return g.dtype == HJ_F64 ? launch_1d_t<double>(g, a, grid_hint, st)
-                           : launch_1d_t<float>(g, a, grid_hint, st);
+  if (g.gen)
+    return g.dtype == HJ_F64 ? launch_1d_t<double, true>(g, a, grid_hint, st)
+                             : launch_1d_t<float, true>(g, a, grid_hint, st);
+  return g.dtype == HJ_F64 ? launch_1d_t<double, false>(g, a, grid_hint, st)
+                           : launch_1d_t<float, false>(g, a, grid_hint, st);
 }
 
 }  // namespace hj

@@ -5,6 +5,9 @@
 // and copies the interior back.  PAPER.md:114-133 (§3.2): the classic sweep.
 // Every kernel also reduces the h^2-scaled residual of the snapshot it reads:
 // s = h2f - (4x - ((W+E)+(S+N))), sum of s^2 per tile -> part[tile].
+// GEN = true: the general constant-coefficient stencil of Eq. 10 — the update
+// and residual of hj_internal.cuh gupd2 / gres2 (reading c23) with the weights held as
+// kernel parameters; everything else (tiles, halo, stores) is unchanged.
 #include <type_traits>
 
 #include "hj_internal.cuh"
@@ -48,16 +51,21 @@ struct R2 {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <typename T, bool MASK>
+template <typename T, bool MASK, bool GEN>
 struct Tile2 {
   T x[8][4];      // current iterate
-  T q[8][4];      // 0.25 * h^2 f
+  T q[8][4];      // 0.25 * h^2 f  (GEN: b / d)
+  T cw[4];        // GEN: weights W, E, S, N
   const T* hxp;   // per-warp smem: frozen W (lx == 0) / E (lx == 7) halo of my 8 rows
   const T* hyp;   // per-warp smem: frozen S (ly == 0) / N (ly == 3) halo of my 4 columns
   uint32_t own;   // MASK (overlapping blocks): bit 4*i+c set if this block owns cell (i, c)
 
   __device__ __forceinline__ bool on(int i, int c) const {
     return !MASK || ((own >> (4 * i + c)) & 1u);
+  }
+  __device__ __forceinline__ T upd(T W, T E, T S, T N, T qq) const {
+    if constexpr (GEN) return gupd2(cw[0], cw[1], cw[2], cw[3], W, E, S, N, qq);
+    else return upd2(W, E, S, N, qq);
   }
 
   // N/S neighbour rows across lane rows: row 0 of the lane below is my row 7's N, row 7 of the
@@ -100,8 +108,11 @@ struct Tile2 {
         const T E = c == 3 ? e : x[i][c + 1];
         const T S = i == 0 ? dn[c] : x[i - 1][c];
         const T N = i == 7 ? up[c] : x[i + 1][c];
-        const double s = res2((double)x[i][c], (double)W, (double)E, (double)S, (double)N,
-                              (double)(T(4) * q[i][c]));
+        const double s =
+            GEN ? gres2((double)cw[0], (double)cw[1], (double)cw[2], (double)cw[3], (double)x[i][c],
+                        (double)W, (double)E, (double)S, (double)N, (double)q[i][c])
+                : res2((double)x[i][c], (double)W, (double)E, (double)S, (double)N,
+                       (double)(T(4) * q[i][c]));
         if (on(i, c)) acc = __fma_rn(s, s, acc);
       }
     }
@@ -132,14 +143,18 @@ struct Tile2 {
         // S = old row i-1, N = old row i+1
         const T S = (i == 0) ? dn[c] : (step > 0 && hi_side ? ohi[c] : x[i - 1][c]);
         const T N = (i == 7) ? up[c] : (step > 0 && !hi_side ? olo[c] : x[i + 1][c]);
-        if constexpr (RES) {
+        if constexpr (RES && GEN) {  // T = double: the residual is the update minus x (c23)
+          nw[c] = upd(W, E, S, N, q[i][c]);
+          const double r = __dsub_rn(nw[c], x[i][c]);
+          if (on(i, c)) acc[c] = __fma_rn(r, r, acc[c]);
+        } else if constexpr (RES) {
           const double sum = __dadd_rn(__dadd_rn(W, E), __dadd_rn(S, N));
           nw[c] = __fma_rn(0.25, sum, q[i][c]);
           const double t = __fma_rn(4.0, x[i][c], -sum);
           const double r = __fma_rn(4.0, q[i][c], -t);
           if (on(i, c)) acc[c] = __fma_rn(r, r, acc[c]);
         } else {
-          nw[c] = upd2(W, E, S, N, q[i][c]);
+          nw[c] = upd(W, E, S, N, q[i][c]);
         }
       }
 #pragma unroll
@@ -155,15 +170,18 @@ struct Tile2 {
 };
 
 // One full 32x32 tile: smem slot -> registers, refill, fused residual, k sub-iterations, store.
-template <typename T, typename C, bool MASK, typename Refill, typename Store>
-__device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __restrict__ sf,
+template <typename T, typename C, bool MASK, bool GEN, typename Refill, typename Store>
+__device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ sx, const T* __restrict__ sf,
                                            T* __restrict__ so, T* __restrict__ hb, int lane, int kk,
                                            double* __restrict__ part, long long t, Refill&& refill,
                                            Store&& store, T* __restrict__ gdst, long long pitch,
                                            int ox0, int ox1, int oy0, int oy1) {
   using V2 = typename VecOf<T>::v2;
   const int lx = lane & 7, ly = lane >> 3;
-  Tile2<T, MASK> tl;
+  Tile2<T, MASK, GEN> tl;
+  if constexpr (GEN) {
+    tl.cw[0] = (T)wt.w; tl.cw[1] = (T)wt.e; tl.cw[2] = (T)wt.s; tl.cw[3] = (T)wt.n;
+  }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {  // 128-bit shared loads
     const int r = 8 * ly + i;
@@ -252,12 +270,12 @@ __device__ __forceinline__ void reg2d_tile(const T* __restrict__ sx, const T* __
 // Persistent kernel over the FULL 32x32 tiles (ntx_full x nty_full of them; ragged edge tiles,
 // if any, are done by smem2d_kernel in edge mode).  Warp w handles full tiles w, w+W, ...;
 // partials are indexed by the global tile index ty*ntx + tx.
-template <typename T, typename C, bool MASK>
+template <typename T, typename C, bool MASK, bool GEN>
 __global__ void __launch_bounds__(C::WARPS * 32, 1)
 reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
              const __grid_constant__ CUtensorMap tmO, T* __restrict__ xout, long long pitch,
              Axis ax, Axis ay, int ntx_full, long long nfull, int ntx, double* __restrict__ part,
-             const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
+             const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt) {
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
   extern __shared__ unsigned char smem_raw[];
@@ -293,8 +311,8 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
     mbar_wait(bar, it & 1);
     const int tx = (int)(u % ntx_full), ty = (int)(u / ntx_full);
     const int x0 = axis_start(ax, tx), y0 = axis_start(ay, ty);
-    reg2d_tile<T, C, MASK>(
-        sx, sf, so, hb, lane, kk, part, (long long)ty * ntx + tx,
+    reg2d_tile<T, C, MASK, GEN>(
+        wt, sx, sf, so, hb, lane, kk, part, (long long)ty * ntx + tx,
         [&] {
           if (lane == 0 && u + nw < nfull) {
             fence_proxy_async();  // generic reads of the slot before the TMA overwrite
@@ -321,11 +339,11 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
 // =============================================================================
 // edge != 0: only the ragged edge tiles — blocks [0, nty) are the last tile column (if nx is
 // ragged), the following blocks the last tile row (if ny is ragged) — for REG2D grids.
-template <typename T>
+template <typename T, bool GEN>
 __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
                               const T* __restrict__ h2f, long long pitch, long long fpitch, int nx,
                               int ny, Axis ax, Axis ay, int edge, double* __restrict__ part,
-                              const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
+                              const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt) {
   const int ntx = ax.nb, nty = ay.nb;
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
@@ -369,9 +387,13 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
   // fused residual of the snapshot
   double s2 = 0.0;
   const int c = (b + 1) * L + (a + 1);
+  const T ww = (T)wt.w, we = (T)wt.e, ws = (T)wt.s, wn = (T)wt.n;
   if (owned) {
-    const double s = res2((double)A[c], (double)A[c - 1], (double)A[c + 1], (double)A[c - L],
-                          (double)A[c + L], (double)(T(4) * rhs[b * Tx + a]));
+    const double s =
+        GEN ? gres2((double)ww, (double)we, (double)ws, (double)wn, (double)A[c], (double)A[c - 1],
+                    (double)A[c + 1], (double)A[c - L], (double)A[c + L], (double)rhs[b * Tx + a])
+            : res2((double)A[c], (double)A[c - 1], (double)A[c + 1], (double)A[c - L],
+                   (double)A[c + L], (double)(T(4) * rhs[b * Tx + a]));
     s2 = s * s;
   }
   s2 = warp_sum(s2);
@@ -387,7 +409,9 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
   T* cur = A;
   T* nxt = B;
   for (int s = 0; s < kk; ++s) {
-    if (active) nxt[c] = upd2(cur[c - 1], cur[c + 1], cur[c - L], cur[c + L], q4);
+    if (active)
+      nxt[c] = GEN ? gupd2(ww, we, ws, wn, cur[c - 1], cur[c + 1], cur[c - L], cur[c + L], q4)
+                   : upd2(cur[c - 1], cur[c + 1], cur[c - L], cur[c + L], q4);
     __syncthreads();
     T* tmp = cur; cur = nxt; nxt = tmp;
   }
@@ -401,11 +425,12 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
 // with 128-bit loads/stores; W/E neighbours by warp shuffle, N/S from the rows held in
 // registers.  Fused residual of the snapshot, one partial per WARP (no CTA barrier).
 // =============================================================================
-template <typename T>
+template <typename T, bool GEN>
 __global__ void __launch_bounds__(128)
 classic2d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restrict__ qarr,
                  long long pitch, long long fpitch, int nx, int ny, int ncb,
-                 double* __restrict__ part, const Ctrl* __restrict__ ctrl, long long max_cycles) {
+                 double* __restrict__ part, const Ctrl* __restrict__ ctrl, long long max_cycles,
+                 Wt2 wt) {
   if (ctrl->done) return;
   const bool write = ctrl->c < max_cycles;
   constexpr int COL0 = 16 / sizeof(T);
@@ -449,6 +474,16 @@ classic2d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __res
       }
     }
   }
+  const T ww = (T)wt.w, we = (T)wt.e, ws = (T)wt.s, wn = (T)wt.n;
+  auto res = [&](T xc, T W, T E, T S, T N, T q) -> double {
+    return GEN ? gres2((double)ww, (double)we, (double)ws, (double)wn, (double)xc, (double)W,
+                       (double)E, (double)S, (double)N, (double)q)
+               : res2((double)xc, (double)W, (double)E, (double)S, (double)N, (double)(T(4) * q));
+  };
+  auto upd = [&](T W, T E, T S, T N, T q) -> T {
+    if constexpr (GEN) return gupd2(ww, we, ws, wn, W, E, S, N, q);
+    else return upd2(W, E, S, N, q);
+  };
   double acc = 0.0;
 #pragma unroll
   for (int r = 1; r <= R; ++r) {
@@ -460,16 +495,14 @@ classic2d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __res
     if (j < ny) {
       T n0 = T(0), n1 = T(0);
       if (v0) {
-        const double s = res2((double)x0[r], (double)w, (double)x1[r], (double)x0[r - 1],
-                              (double)x0[r + 1], (double)(T(4) * f0[r - 1]));
+        const double s = res(x0[r], w, x1[r], x0[r - 1], x0[r + 1], f0[r - 1]);
         acc = __fma_rn(s, s, acc);
-        n0 = upd2(w, x1[r], x0[r - 1], x0[r + 1], f0[r - 1]);
+        n0 = upd(w, x1[r], x0[r - 1], x0[r + 1], f0[r - 1]);
       }
       if (v1) {
-        const double s = res2((double)x1[r], (double)x0[r], (double)e, (double)x1[r - 1],
-                              (double)x1[r + 1], (double)(T(4) * f1[r - 1]));
+        const double s = res(x1[r], x0[r], e, x1[r - 1], x1[r + 1], f1[r - 1]);
         acc = __fma_rn(s, s, acc);
-        n1 = upd2(x0[r], e, x1[r - 1], x1[r + 1], f1[r - 1]);
+        n1 = upd(x0[r], e, x1[r - 1], x1[r + 1], f1[r - 1]);
       }
       if (write) {
         T* dst = xout + (j + 1) * pitch + COL0 + i;
@@ -482,8 +515,9 @@ classic2d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __res
   if (lane == 0) part[(rb * ncb + cb) * 4 + warp] = acc;
 }
 
-template <typename T>
+template <typename T, bool GEN>
 cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
+  const Wt2 wt{g.wt[0], g.wt[1], g.wt[2], g.wt[3]};
   const size_t smem_paper = sizeof(T) * (2 * size_t(g.tx + 2) * (g.ty + 2) + size_t(g.tx) * g.ty);
   if (g.kernel_kind == K_REG2D) {
     // o = 0: the full 32x32 tiles here, ragged edge tiles by smem2d in edge mode;
@@ -496,26 +530,26 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
         using C = decltype(cfg);
         long long ctas = (nfull + C::WARPS - 1) / C::WARPS;
         if (ctas > grid_hint) ctas = grid_hint;
-        reg2d_kernel<T, C, decltype(mask)::value><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
+        reg2d_kernel<T, C, decltype(mask)::value, GEN><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
             *a.tm_in, *a.tm_f, *a.tm_out, (T*)a.xout, g.pitch, g.ax, g.ay, (int)ntx_full, nfull,
-            (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles);
+            (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles, wt);
       };
       if (ovl) go(R2<T>{}, std::true_type{});
       else go(R2<T>{}, std::false_type{});
     }
     const long long nedge = g.ntiles - nfull;
     if (nedge > 0)
-      smem2d_kernel<T><<<(unsigned)nedge, dim3(32, 32), smem_paper, st>>>(
+      smem2d_kernel<T, GEN><<<(unsigned)nedge, dim3(32, 32), smem_paper, st>>>(
           (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
-          g.ax, g.ay, 1, a.part, a.ctrl, g.k, a.max_cycles);
+          g.ax, g.ay, 1, a.part, a.ctrl, g.k, a.max_cycles, wt);
   } else if (g.kernel_kind == K_SMEM2D) {
-    smem2d_kernel<T><<<(unsigned)g.ntiles, dim3(g.tx, g.ty), smem_paper, st>>>(
+    smem2d_kernel<T, GEN><<<(unsigned)g.ntiles, dim3(g.tx, g.ty), smem_paper, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
-        g.ax, g.ay, 0, a.part, a.ctrl, g.k, a.max_cycles);
+        g.ax, g.ay, 0, a.part, a.ctrl, g.k, a.max_cycles, wt);
   } else {
-    classic2d_kernel<T><<<(unsigned)(g.ntx * g.nty), 128, 0, st>>>(
+    classic2d_kernel<T, GEN><<<(unsigned)(g.ntx * g.nty), 128, 0, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
-        (int)g.ntx, a.part, a.ctrl, a.max_cycles);
+        (int)g.ntx, a.part, a.ctrl, a.max_cycles, wt);
   }
   return cudaGetLastError();
 }
@@ -523,31 +557,31 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
 }  // namespace
 
 
-template <typename T, typename C>
+template <typename T, typename C, bool GEN>
 cudaError_t cfg2() {
-  cudaError_t e = cudaFuncSetAttribute(reg2d_kernel<T, C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)C::SMEM);
+  cudaError_t e = cudaFuncSetAttribute(reg2d_kernel<T, C, false, GEN>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(reg2d_kernel<T, C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-}
-
-template <typename T, typename C>
-cudaError_t cfg2u() {  // unmasked instantiation only
-  return cudaFuncSetAttribute(reg2d_kernel<T, C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  e = cudaFuncSetAttribute(reg2d_kernel<T, C, true, GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)C::SMEM);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(smem2d_kernel<T, GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
 cudaError_t configure_2d() {
   cudaError_t e;
-  if ((e = cfg2<double, R2<double>>()) != cudaSuccess) return e;
-  if ((e = cfg2<float, R2<float>>()) != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(smem2d_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(smem2d_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if ((e = cfg2<double, R2<double>, false>()) != cudaSuccess) return e;
+  if ((e = cfg2<float, R2<float>, false>()) != cudaSuccess) return e;
+  if ((e = cfg2<double, R2<double>, true>()) != cudaSuccess) return e;
+  return cfg2<float, R2<float>, true>();
 }
 
 cudaError_t launch_cycle_2d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
-  return g.dtype == HJ_F64 ? launch_2d_t<double>(g, a, grid_hint, st)
-                           : launch_2d_t<float>(g, a, grid_hint, st);
+  if (g.gen)
+    return g.dtype == HJ_F64 ? launch_2d_t<double, true>(g, a, grid_hint, st)
+                             : launch_2d_t<float, true>(g, a, grid_hint, st);
+  return g.dtype == HJ_F64 ? launch_2d_t<double, false>(g, a, grid_hint, st)
+                           : launch_2d_t<float, false>(g, a, grid_hint, st);
 }
 
 }  // namespace hj

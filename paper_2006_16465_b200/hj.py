@@ -30,7 +30,12 @@ _P = ctypes.c_void_p
 
 class hj_problem(ctypes.Structure):
     _fields_ = [("dim", ctypes.c_int32), ("nx", ctypes.c_int64), ("ny", ctypes.c_int64),
-                ("h", ctypes.c_double), ("f", _P), ("bc", _P), ("x0", _P)]
+                ("h", ctypes.c_double), ("f", _P), ("bc", _P), ("x0", _P), ("stencil", _P)]
+
+
+def _nstencil(dim, nx, ny):
+    """Length of hj_problem.stencil: 2D {a, c, e, f, d}; 1D planes [a | d | c] (DESIGN.md c23)."""
+    return 3 * nx * ny if dim == 1 else 5
 
 
 class hj_params(ctypes.Structure):
@@ -135,16 +140,18 @@ def _hp(a):
     return None if a is None else a.ctypes.data
 
 
-def jacobi_solve(dim, nx, ny, h, f, bc=None, x0=None, *, history=True, **params):
-    """Host-buffer solve (H2D/D2H inside).  Returns dict(x, history, cycles, converged, status, ...)."""
+def jacobi_solve(dim, nx, ny, h, f, bc=None, x0=None, *, history=True, stencil=None, **params):
+    """Host-buffer solve (H2D/D2H inside).  Returns dict(x, history, cycles, converged, status, ...).
+    ``stencil``: general coefficients (numpy; hj_problem.stencil), f is then b and h is unused."""
     n = nx * ny
     f = _host(f, n, "f")
     bc = _host(bc, 2 * ny if dim == 1 else 2 * nx + 2 * ny, "bc")   # dim 1: per problem
     x0 = _host(x0, n, "x0")
+    stencil = _host(stencil, _nstencil(dim, nx, ny), "stencil")
     prm = make_params(**params)
     x = np.empty(n)
     hist = np.empty(prm.max_cycles + 1) if history else None
-    pb = hj_problem(dim, nx, ny, float(h), _hp(f), _hp(bc), _hp(x0))
+    pb = hj_problem(dim, nx, ny, float(h), _hp(f), _hp(bc), _hp(x0), _hp(stencil))
     res = hj_result(x.ctypes.data, _hp(hist), 0, 0, 0.0, 0.0, 0.0, 0.0)
     st = _check(lib().jacobi_solve(ctypes.byref(pb), ctypes.byref(prm), ctypes.byref(res)),
                 ok=(HJ_OK, HJ_NOT_CONVERGED, HJ_ERR_NUMERIC))
@@ -162,14 +169,15 @@ def _dptr(t):
     return None if t is None else t.data_ptr()
 
 
-def jacobi_solve_device(dim, nx, ny, h, f, bc=None, x0=None, *, history=True, stream=None, **params):
-    """Device solve on torch CUDA tensors (float64).  Returns torch tensors."""
+def jacobi_solve_device(dim, nx, ny, h, f, bc=None, x0=None, *, history=True, stream=None,
+                        stencil=None, **params):
+    """Device solve on torch CUDA tensors (float64, stencil included).  Returns torch tensors."""
     import torch
     prm = make_params(**params)
     dev = f.device
     x = torch.empty(nx * ny, dtype=torch.float64, device=dev)
     hist = torch.empty(prm.max_cycles + 1, dtype=torch.float64, device=dev) if history else None
-    pb = hj_problem(dim, nx, ny, float(h), _dptr(f), _dptr(bc), _dptr(x0))
+    pb = hj_problem(dim, nx, ny, float(h), _dptr(f), _dptr(bc), _dptr(x0), _dptr(stencil))
     res = hj_result(_dptr(x), _dptr(hist), 0, 0, 0.0, 0.0, 0.0, 0.0)
     s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
     st = _check(lib().jacobi_solve_device(ctypes.byref(pb), ctypes.byref(prm), ctypes.byref(res), s),
@@ -180,7 +188,7 @@ def jacobi_solve_device(dim, nx, ny, h, f, bc=None, x0=None, *, history=True, st
 
 def hj_resource_figures(dim, nx, ny, **params):
     prm = make_params(**params)
-    pb = hj_problem(dim, nx, ny, 1.0 / (nx + 1), None, None, None)
+    pb = hj_problem(dim, nx, ny, 1.0 / (nx + 1), None, None, None, None)
     a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
     _check(lib().hj_resource_figures(ctypes.byref(pb), ctypes.byref(prm), ctypes.byref(a),
                                      ctypes.byref(b), ctypes.byref(c)), ok=(HJ_OK,))
@@ -194,16 +202,17 @@ def hj_nccl_unique_id() -> bytes:
 
 
 def jacobi_solve_dist(nx, ny, h, f_local, bc, x0_local, *, rank, nranks, nccl_id: bytes,
-                      row_begin, row_end, history=True, **params):
+                      row_begin, row_end, history=True, stencil=None, **params):
     """Row-slab solve on this rank's GPU (host buffers of the local rows)."""
     nloc = nx * (row_end - row_begin)
     f = _host(f_local, nloc, "f")
     bc = _host(bc, 2 * nx + 2 * ny, "bc")
     x0 = _host(x0_local, nloc, "x0")
+    stencil = _host(stencil, 5, "stencil")
     prm = make_params(**params)
     x = np.empty(nloc)
     hist = np.empty(prm.max_cycles + 1) if history else None
-    pb = hj_problem(2, nx, ny, float(h), _hp(f), _hp(bc), _hp(x0))
+    pb = hj_problem(2, nx, ny, float(h), _hp(f), _hp(bc), _hp(x0), _hp(stencil))
     res = hj_result(x.ctypes.data, _hp(hist), 0, 0, 0.0, 0.0, 0.0, 0.0)
     idbuf = ctypes.create_string_buffer(nccl_id, 128)
     d = hj_dist(rank, nranks, ctypes.cast(idbuf, ctypes.c_char_p), row_begin, row_end)
@@ -216,14 +225,16 @@ def jacobi_solve_dist(nx, ny, h, f_local, bc, x0_local, *, rank, nranks, nccl_id
 class Plan:
     """hj_plan_*: device-resident state for repeated cycles (bench, resume)."""
 
-    def __init__(self, dim, nx, ny, h, f, bc=None, x0=None, *, stream=None, **params):
+    def __init__(self, dim, nx, ny, h, f, bc=None, x0=None, *, stream=None, stencil=None, **params):
         import torch
         self.prm = make_params(**params)
         self.dim, self.nx, self.ny = dim, nx, ny
-        self._keep = (f, bc, x0)
+        if stencil is not None and not isinstance(stencil, torch.Tensor):
+            stencil = torch.as_tensor(np.ascontiguousarray(stencil, dtype=np.float64), device=f.device)
+        self._keep = (f, bc, x0, stencil)
         self.stream = stream if stream is not None else torch.cuda.current_stream(f.device).cuda_stream
         torch.cuda.synchronize(f.device)   # inputs may have been written on another stream
-        pb = hj_problem(dim, nx, ny, float(h), _dptr(f), _dptr(bc), _dptr(x0))
+        pb = hj_problem(dim, nx, ny, float(h), _dptr(f), _dptr(bc), _dptr(x0), _dptr(stencil))
         self._p = _P()
         self._create(pb)
         self.launches_per_cycle_static = lib().hj_plan_launches_per_cycle(self._p)
@@ -272,11 +283,12 @@ class DistPlan(Plan):
     tensors f, x0 of the local rows; bc the full ring).  Collective over all ranks."""
 
     def __init__(self, nx, ny, h, f, bc, x0, *, rank, nranks, nccl_id: bytes, row_begin, row_end,
-                 stream=None, **params):
+                 stream=None, stencil=None, **params):
         self._dist_args = (rank, nranks, nccl_id, row_begin, row_end)
         self.ny_global = ny
         # the problem handed to the C-ABI carries the GLOBAL ny; solve() views the local rows
-        super().__init__(2, nx, row_end - row_begin, h, f, bc, x0, stream=stream, **params)
+        super().__init__(2, nx, row_end - row_begin, h, f, bc, x0, stream=stream, stencil=stencil,
+                         **params)
 
     def _create(self, pb):
         rank, nranks, nccl_id, rb, re = self._dist_args
