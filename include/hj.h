@@ -62,7 +62,9 @@ typedef enum {
   HJ_ERR_NUMERIC = 4,        /* NaN/Inf residual                                               */
   HJ_ERR_CUDA = 5,
   HJ_ERR_NCCL = 6,
-  HJ_ERR_OOM = 7
+  HJ_ERR_OOM = 7,
+  HJ_ERR_PEER = 8            /* peer transport: a rank did not signal within HJ_PEER_TIMEOUT_S
+                                (default 30 s), or plan used before hj_plan_peer_attach        */
 } hj_status;
 
 typedef enum { HJ_F64 = 0, HJ_F32 = 1 } hj_dtype;
@@ -175,6 +177,27 @@ hj_status hj_plan_create_dist(const hj_problem *problem, const hj_params *params
  * single-GPU solve for any nranks (tile rows never straddle slabs). */
 hj_status jacobi_solve_dist(const hj_problem *problem, const hj_params *params,
                             hj_result *result, const hj_dist *dist);
+
+/* ---- multi-GPU without NCCL: the peer-memory transport ----
+ * Same row slabs and bitwise guarantees as above, but the per-cycle exchange is done by the
+ * library's own kernels through CUDA IPC mappings of the neighbours' buffers (NVLink/NVSwitch
+ * stores between GPUs; processes sharing one GPU also work): rows 1 and R of the new iterate are
+ * stored into the neighbours' ghost rows, each rank's residual row sums are stored into every
+ * rank's residual vector, and the finalize kernel signals every rank (fence.sys + atomic) and
+ * waits for all signals of the cycle (bounded spin; HJ_ERR_PEER after HJ_PEER_TIMEOUT_S).
+ * Usage (every rank, one process per GPU):
+ *   hj_plan_create_peer(...)              dist->nccl_id is ignored (may be NULL)
+ *   hj_plan_peer_export(plan, blob)       HJ_PEER_HANDLE_BYTES bytes
+ *   -- the caller all-gathers the blobs in rank order (e.g. torch.distributed) --
+ *   hj_plan_peer_attach(plan, blobs)      opens the mappings and runs the collective reset
+ * after which hj_plan_run / hj_plan_solve work as for any plan.  hj_plan_reset and
+ * hj_plan_destroy are collective: call them on every rank (destroy only after every rank has
+ * finished its last run).  Problem pointers as for hj_plan_create_dist. */
+#define HJ_PEER_HANDLE_BYTES 512
+hj_status hj_plan_create_peer(const hj_problem *problem, const hj_params *params,
+                              const hj_dist *dist, void *cuda_stream, hj_plan **plan);
+hj_status hj_plan_peer_export(const hj_plan *plan, void *handle_out);
+hj_status hj_plan_peer_attach(hj_plan *plan, const void *all_handles);
 
 /* Resource figures of the paper: tiles = the paper's operational block count (
  * with overlap Eq. 8/13, ceiling when inexact), threads = tiles*tile_x*tile_y

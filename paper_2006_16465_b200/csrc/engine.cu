@@ -130,29 +130,74 @@ __global__ void extract_kernel(const T* __restrict__ X, long long pitch, int dim
 }
 
 // R[rg_offset + g] = sum_{p < ppr} part[g*ppr + p], fixed order (lane-strided, then an xor tree).
+// Peer transport (d.n > 0): the sum goes to slot rg_offset + g of EVERY rank's vector (remote
+// stores), fenced at system scope before the finalize signal publishes it.  The vector is double
+// buffered by cycle parity (offset (c & 1) * rp_stride): a rank signals cycle c before it reads
+// its vector, so a faster rank may already store cycle c+1's sums — into the other half.
 __global__ void rowsum_kernel(const double* __restrict__ part, long long ppr, long long nrg,
-                              long long rg_offset, double* __restrict__ R, const Ctrl* __restrict__ ctrl) {
+                              long long rg_offset, double* __restrict__ R, const Ctrl* __restrict__ ctrl,
+                              PeerDsts d, long long rp_stride) {
   if (ctrl->done) return;
+  rg_offset += (ctrl->c & 1) * rp_stride;
   const long long g = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (g >= nrg) return;
   double s = 0.0;
   for (long long p = lane; p < ppr; p += 32) s += part[g * ppr + p];
   s = warp_sum(s);
-  if (lane == 0) R[rg_offset + g] = s;
+  if (d.n == 0) {
+    if (lane == 0) R[rg_offset + g] = s;
+    return;
+  }
+  for (int r = lane; r < d.n; r += 32) d.p[r][rg_offset + g] = s;
+  __threadfence_system();
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 // S_c = sum of R (fixed order); history; the stopping test of DESIGN.md §3 (c1, c14):
 // c = 0: converged iff S_0 == 0 (or the test holds with an explicit r_0 / absolute mode);
 // c >= 1: converged iff sqrt(S_c) <= tol * sqrt(S_0)  (absolute: sqrt(S_c)/h^2 <= tol).
 // h2 here is Geom::rdiv (h^2 for the Poisson problem; DESIGN.md c3, c23).
+// Peer transport (ps.n > 0): first signal every rank and wait until all nranks signals of this
+// cycle arrived (their halo and rowsum stores are then visible), then read R from L2 (__ldcg).
 __global__ void finalize_kernel(const double* __restrict__ R, long long nrg, Ctrl* __restrict__ ctrl,
                                 double* __restrict__ hist, long long hist_cap, double h2, double tol,
-                                int tol_mode, double ref_residual, long long max_cycles) {
+                                int tol_mode, double ref_residual, long long max_cycles, PeerSync ps,
+                                long long rp_stride) {
   if (ctrl->done) return;
+  R += (ctrl->c & 1) * rp_stride;
   __shared__ double ws[32];
+  if (ps.n > 0) {
+    __shared__ int timed_out;
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int r = 0; r < ps.n; ++r) atomicAdd_system(ps.flag[r], 1ULL);
+      const unsigned long long want = ctrl->sig0 + (unsigned long long)ps.n * (unsigned long long)(ctrl->c + 1);
+      const unsigned long long t0 = gtimer();
+      timed_out = 0;
+      for (;;) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(ps.own) : "memory");
+        if (v >= want) break;
+        if ((long long)(gtimer() - t0) > ps.timeout_ns) { timed_out = 1; break; }
+        __nanosleep(200);
+      }
+      if (timed_out) {
+        ctrl->status = HJ_ERR_PEER;
+        ctrl->done = 1;
+        ctrl->c_done = ctrl->c;
+      }
+    }
+    __syncthreads();
+    if (timed_out) return;
+  }
   double s = 0.0;
-  for (long long p = threadIdx.x; p < nrg; p += blockDim.x) s += R[p];
+  for (long long p = threadIdx.x; p < nrg; p += blockDim.x) s += __ldcg(R + p);
   s = warp_sum(s);
   if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
   __syncthreads();
@@ -438,13 +483,20 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
     PCK(cudaMalloc(&P->WR, fbytes));
   }
   PCK(cudaMalloc(&P->part, sizeof(double) * (g.nparts + 1)));
-  PCK(cudaMalloc(&P->rowpart, sizeof(double) * (g.nrg_global + 1)));
+  const bool peer = di && di->transport == 1;
+  P->rp_stride = peer ? g.nrg_global + 1 : 0;   // peer: two halves, by cycle parity
+  PCK(cudaMalloc(&P->rowpart, sizeof(double) * (g.nrg_global + 1) * (peer ? 2 : 1)));
   P->rowsum_dst = P->rowpart;
   if (di) {
     PCK(cudaMalloc(&P->rowpart_local, sizeof(double) * (g.nrg_global + 1)));
     PCK(cudaMemsetAsync(P->rowpart_local, 0, sizeof(double) * (g.nrg_global + 1), st));
     P->rowsum_dst = P->rowpart_local;
-    s = dist_create(P, di);
+    if (di->transport == 1) {
+      P->rowsum_dst = P->rowpart;   // peer: rowsum stores into every rank's rowpart itself
+      s = peer_create(P, di);
+    } else {
+      s = dist_create(P, di);
+    }
     if (s != HJ_OK) return fail(s);
   }
   PCK(cudaMalloc(&P->hist, sizeof(double) * P->hist_cap));
@@ -461,7 +513,7 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
   PCK(cudaMalloc(&P->x0_d, sizeof(double) * nloc));
   if (pb->x0) PCK(cudaMemcpyAsync(P->x0_d, pb->x0, sizeof(double) * nloc, cudaMemcpyDefault, st));
   else PCK(cudaMemsetAsync(P->x0_d, 0, sizeof(double) * nloc, st));
-  PCK(cudaMemsetAsync(P->rowpart, 0, sizeof(double) * (g.nrg_global + 1), st));
+  PCK(cudaMemsetAsync(P->rowpart, 0, sizeof(double) * (g.nrg_global + 1) * (peer ? 2 : 1), st));
   PCK(cudaMemsetAsync(P->part, 0, sizeof(double) * (g.nparts + 1), st));
   if (g.gen) {
     // general coefficients (c23): device copy of the stencil (host or device pointer), checked on
@@ -556,6 +608,7 @@ hj_status plan_reset(hj_plan* P) {
   *P->ctrl_h = c0;
   HJ_CUDA(cudaMemcpyAsync(P->ctrl, P->ctrl_h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
   if (P->dist) HJ_TRY(dist_initial_exchange(P));
+  if (P->peer) HJ_TRY(peer_reset(P));
   HJ_CUDA(cudaStreamSynchronize(st));
   P->c_host = 0;
   return HJ_OK;
@@ -568,6 +621,7 @@ int launches_per_cycle(const hj_plan* P) {
     const long long nfull = (g.nx / 32) * (g.ny / 32);
     n = (nfull > 0 ? 1 : 0) + (g.ntiles > nfull ? 1 : 0) + 2;
   }
+  if (P->peer && peer_halo_launches(P)) n += 1;  // peer_halo_kernel
   return n;
 }
 
@@ -607,14 +661,20 @@ hj_status launch_cycle(hj_plan* P, int p, bool timed, float* acc_ms) {
   }
   if (timed) HJ_CUDA(cudaEventRecord(e1, st));
   if (P->dist) HJ_TRY(dist_halo_exchange(P, p ^ 1));
+  PeerDsts pd{};
+  PeerSync ps{};
+  if (P->peer) {
+    HJ_TRY(peer_halo(P, p ^ 1));
+    peer_cycle_args(P, &pd, &ps);
+  }
   const int wpb = 8;
   rowsum_kernel<<<(unsigned)((g.nrg_local + wpb - 1) / wpb), 32 * wpb, 0, st>>>(
-      P->part, g.parts_per_row, g.nrg_local, g.rg_offset, P->rowsum_dst, P->ctrl);
+      P->part, g.parts_per_row, g.nrg_local, g.rg_offset, P->rowsum_dst, P->ctrl, pd, P->rp_stride);
   HJ_CUDA(cudaGetLastError());
   if (P->dist) HJ_TRY(dist_allreduce(P));
   finalize_kernel<<<1, 1024, 0, st>>>(P->rowpart, g.nrg_global, P->ctrl, P->hist, P->hist_cap, g.rdiv,
                                       P->prm.tol, (int)P->prm.tol_mode, P->prm.ref_residual,
-                                      P->prm.max_cycles);
+                                      P->prm.max_cycles, ps, P->rp_stride);
   HJ_CUDA(cudaGetLastError());
   return HJ_OK;
 }
@@ -652,6 +712,7 @@ static hj_status get_graph(hj_plan* P, int G, cudaGraphExec_t* out) {
 
 hj_status plan_run(hj_plan* P, long long ncycles, float* kernel_ms) {
   if (ncycles < 0) { set_error("ncycles must be >= 0"); return HJ_ERR_INVALID_ARG; }
+  if (P->peer && !peer_attached(P)) { set_error("peer plan used before hj_plan_peer_attach"); return HJ_ERR_PEER; }
   if (kernel_ms) {
     // eager launches, CUDA events around every cycle kernel, one synchronisation at the end
     *kernel_ms = 0.f;
@@ -687,6 +748,7 @@ hj_status plan_run(hj_plan* P, long long ncycles, float* kernel_ms) {
 
 hj_status plan_solve(hj_plan* P, hj_result* res, double* x_dev, double* hist_dev) {
   const Geom& g = P->g;
+  if (P->peer && !peer_attached(P)) { set_error("peer plan used before hj_plan_peer_attach"); return HJ_ERR_PEER; }
   cudaStream_t st = P->stream;
   HJ_CUDA(cudaEventRecord(P->ev0, st));
   if (P->c_host & 1) {  // graphs start at even parity
@@ -734,6 +796,7 @@ void plan_free(hj_plan* P) {
   if (!P) return;
   for (auto& kv : P->graphs) cudaGraphExecDestroy(kv.second);
   if (P->dist) dist_free(P);
+  if (P->peer) peer_free(P);
   cudaFree(P->X[0]);
   cudaFree(P->X[1]);
   cudaFree(P->H2F);

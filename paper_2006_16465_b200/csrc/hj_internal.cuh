@@ -41,6 +41,7 @@ struct Ctrl {
   int pad;
   double sqrtS0;        // sqrt(S_0) used by the relative test (or ref_residual * h^2)
   double S0, S_last;    // h^2-scaled squared residuals
+  unsigned long long sig0;  // peer transport: own signal counter at the last reset
 };
 
 // Subdomains along one axis (0-based interior indices; §3.5, §4.3; DESIGN.md c10, c21).

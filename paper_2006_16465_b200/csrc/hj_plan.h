@@ -10,13 +10,28 @@
 #include "hj_internal.cuh"
 
 struct DistState;  // dist.cu
+struct PeerState;  // peer.cu
 
 namespace hj {
 
 struct DistInfo {
   int rank, nranks;
   long long row_begin, row_end;
-  const char* nccl_id;  // 128 bytes
+  const char* nccl_id;  // 128 bytes (NCCL transport)
+  int transport;        // 0: NCCL (dist.cu), 1: peer memory over CUDA IPC (peer.cu)
+};
+
+// Peer transport (peer.cu): every rank's residual-row vector and signal flags, as kernel params.
+constexpr int HJ_MAX_RANKS = 64;
+struct PeerDsts {   // rowsum writes its row-group sums into every rank's rowpart
+  double* p[HJ_MAX_RANKS];
+  int n;            // 0: single destination (the rowsum_kernel R argument)
+};
+struct PeerSync {   // finalize: signal every rank, then wait for all signals of this cycle
+  unsigned long long* flag[HJ_MAX_RANKS];
+  unsigned long long* own;
+  int n;            // 0: no synchronisation (one GPU / NCCL)
+  long long timeout_ns;
 };
 
 }  // namespace hj
@@ -34,6 +49,7 @@ struct hj_plan {
   void* WR = nullptr;               //                          T(-c_i/d_i)
   double* part = nullptr;
   double* rowpart = nullptr;        // per row group sums, global length (input of finalize)
+  long long rp_stride = 0;          // peer transport: rowpart has two halves (cycle parity)
   double* rowpart_local = nullptr;  // dist: this rank's row groups, zeros elsewhere
   double* rowsum_dst = nullptr;     // where rowsum writes (rowpart, or rowpart_local in dist)
   double* hist = nullptr;
@@ -51,6 +67,7 @@ struct hj_plan {
   std::vector<cudaEvent_t> evpool;  // timed runs: (start, end) per cycle kernel
   int evused = 0;
   DistState* dist = nullptr;
+  PeerState* peer = nullptr;
 };
 
 namespace hj {
@@ -74,4 +91,12 @@ hj_status dist_halo_exchange(hj_plan* P, int buf);
 hj_status dist_allreduce(hj_plan* P);
 void dist_free(hj_plan* P);
 
+// peer.cu
+hj_status peer_create(hj_plan* P, const DistInfo* di);
+bool peer_attached(const hj_plan* P);
+int peer_halo_launches(const hj_plan* P);       // 1 if this rank has a neighbour, else 0
+hj_status peer_reset(hj_plan* P);                 // collective: device barriers + initial halos
+hj_status peer_halo(hj_plan* P, int buf);          // push rows 1 and R of X[buf] to the neighbours
+void peer_cycle_args(const hj_plan* P, PeerDsts* d, PeerSync* s);
+void peer_free(hj_plan* P);
 }  // namespace hj

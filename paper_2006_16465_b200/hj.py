@@ -93,6 +93,9 @@ def lib():
                            ("hj_nccl_unique_id", [ctypes.c_char_p]),
                            ("jacobi_solve_dist", [pp, pr, res, ctypes.POINTER(hj_dist)]),
                            ("hj_plan_create_dist", [pp, pr, ctypes.POINTER(hj_dist), _P, ctypes.POINTER(_P)]),
+                           ("hj_plan_create_peer", [pp, pr, ctypes.POINTER(hj_dist), _P, ctypes.POINTER(_P)]),
+                           ("hj_plan_peer_export", [_P, _P]),
+                           ("hj_plan_peer_attach", [_P, _P]),
                            ("hj_resource_figures", [pp, pr, ctypes.POINTER(ctypes.c_int64),
                                                     ctypes.POINTER(ctypes.c_int64),
                                                     ctypes.POINTER(ctypes.c_int64)])]:
@@ -297,3 +300,50 @@ class DistPlan(Plan):
         d = hj_dist(rank, nranks, ctypes.cast(self._idbuf, ctypes.c_char_p), rb, re)
         _check(lib().hj_plan_create_dist(ctypes.byref(pb), ctypes.byref(self.prm), ctypes.byref(d),
                                          self.stream, ctypes.byref(self._p)), ok=(HJ_OK,))
+
+
+PEER_HANDLE_BYTES = 512   # HJ_PEER_HANDLE_BYTES
+
+
+class PeerPlan(Plan):
+    """hj_plan_create_peer: this rank's row slab with the peer-memory transport (CUDA IPC; the
+    halo rows, residual row sums and per-cycle signals are stored by the library's kernels into
+    the other ranks' buffers — no NCCL).  After construction call ``connect()`` on every rank
+    (``allgather(bytes) -> list[bytes]`` in rank order; default: torch.distributed)."""
+
+    def __init__(self, nx, ny, h, f, bc, x0, *, rank, nranks, row_begin, row_end, stream=None,
+                 stencil=None, **params):
+        self._dist_args = (rank, nranks, row_begin, row_end)
+        self.ny_global = ny
+        super().__init__(2, nx, row_end - row_begin, h, f, bc, x0, stream=stream, stencil=stencil,
+                         **params)
+
+    def _create(self, pb):
+        rank, nranks, rb, re = self._dist_args
+        pb.ny = self.ny_global
+        d = hj_dist(rank, nranks, None, rb, re)
+        _check(lib().hj_plan_create_peer(ctypes.byref(pb), ctypes.byref(self.prm), ctypes.byref(d),
+                                         self.stream, ctypes.byref(self._p)), ok=(HJ_OK,))
+
+    def export(self) -> bytes:
+        buf = ctypes.create_string_buffer(PEER_HANDLE_BYTES)
+        _check(lib().hj_plan_peer_export(self._p, buf), ok=(HJ_OK,))
+        return buf.raw
+
+    def attach(self, blobs):
+        """blobs: every rank's export() in rank order.  Collective (runs the initial exchange)."""
+        allb = b"".join(bytes(b) for b in blobs)
+        if len(allb) != PEER_HANDLE_BYTES * self._dist_args[1]:
+            raise ValueError("attach needs one blob per rank")
+        buf = ctypes.create_string_buffer(allb, len(allb))
+        _check(lib().hj_plan_peer_attach(self._p, buf), ok=(HJ_OK,))
+        self.launches_per_cycle_static = lib().hj_plan_launches_per_cycle(self._p)
+
+    def connect(self, allgather=None):
+        if allgather is None:
+            import torch.distributed as dist
+            def allgather(b):
+                out = [None] * dist.get_world_size()
+                dist.all_gather_object(out, b)
+                return out
+        self.attach(allgather(self.export()))

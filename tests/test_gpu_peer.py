@@ -1,0 +1,84 @@
+"""The peer-memory transport (CUDA IPC, no NCCL) with 2 and 3 REAL ranks: separate processes
+sharing the one GPU of this box (CUDA IPC works between processes on the same device; NCCL
+refuses duplicate GPUs, so this is the only multi-rank data-path test that runs here).
+
+Bar (c18): every rank's rows, the history and the cycle count are bitwise equal to
+the single-GPU solve of the same problem."""
+import multiprocessing as mp
+import os
+
+import numpy as np
+import pytest
+
+from paper_2006_16465_b200 import hj
+from paper_2006_16465_b200.inputs import make_general, make_problem
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(case, nranks):
+    from tests import _peer_worker
+    ctx = mp.get_context("spawn")
+    os.environ.setdefault("HJ_PEER_TIMEOUT_S", "60")
+    up, out = ctx.Queue(), ctx.Queue()
+    downs = [ctx.Queue() for _ in range(nranks)]
+    procs = [ctx.Process(target=_peer_worker.run, args=(r, nranks, case, up, downs[r], out)) for r in range(nranks)]
+    for p in procs:
+        p.start()
+    try:
+        blobs = {}
+        while len(blobs) < nranks:
+            item = up.get(timeout=300)
+            blobs[item[0]] = item[1]
+        for q in downs:
+            q.put([blobs[r] for r in range(nranks)])
+        res = [out.get(timeout=600) for _ in range(nranks)]
+        for q in downs:
+            q.put("done")
+        for p in procs:
+            p.join(timeout=120)
+    finally:
+        for p in procs:
+            if p.is_alive():
+                p.kill()
+    errs = [r["error"] for r in res if "error" in r]
+    assert not errs, errs[0]
+    return sorted(res, key=lambda r: r["rank"])
+
+
+def _single(case):
+    nx, ny = case["nx"], case["ny"]
+    p = make_general(case["recipe"], 2, nx, ny) if case.get("general") else make_problem(case["recipe"], 2, nx, ny)
+    prm = dict(mode=case["mode"], tile=case["tile"], k=case["k"], tol=case["tol"], max_cycles=case["max_cycles"],
+               dtype=case.get("dtype", "f64"))
+    if case["mode"] == "classic":
+        prm.pop("tile"); prm["k"] = 1
+    return hj.jacobi_solve(2, nx, ny, p["h"], p["f"], p["bc"], p["x0"], stencil=p.get("stencil"), **prm)
+
+
+CASES = [
+    dict(name="reg2d_R_fixed", recipe="R", nx=128, ny=192, mode="hier", tile=(32, 32), k=5, tol=0.0, max_cycles=7),
+    dict(name="reg2d_P_tol", recipe="P", nx=160, ny=128, mode="hier", tile=(32, 32), k=16, tol=1e-6, max_cycles=100000),
+    dict(name="smem_ragged_f32", recipe="R", nx=100, ny=96, mode="hier", tile=(16, 16), k=4, tol=0.0, max_cycles=5,
+         dtype="f32"),
+    dict(name="classic", recipe="R", nx=300, ny=64, mode="classic", tile=(1, 1), k=1, tol=0.0, max_cycles=9),
+    dict(name="general_aniso", recipe="A", general=True, nx=128, ny=96, mode="hier", tile=(32, 32), k=8, tol=1e-5,
+         max_cycles=100000, rerun=True),
+]
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_peer_transport_bitwise_vs_single_gpu(case, nranks):
+    ref = _single(case)
+    res = _run(case, nranks)
+    xr = np.asarray(ref["x"]).reshape(case["ny"], case["nx"])
+    for r in res:
+        assert r["status"] == ref["status"]
+        assert r["cycles"] == ref["cycles"]
+        assert np.array_equal(r["x"].reshape(r["re"] - r["rb"], case["nx"]), xr[r["rb"]:r["re"]])
+        assert np.array_equal(r["hist"], ref["history"])
+        if case.get("rerun"):   # collective reset, second solve identical
+            assert r["cycles2"] == ref["cycles"]
+            assert np.array_equal(r["x2"].reshape(r["re"] - r["rb"], case["nx"]), xr[r["rb"]:r["re"]])
+    assert res[0]["lpc"] >= 4   # cycle kernel(s) + halo + rowsum + finalize
