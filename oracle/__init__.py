@@ -61,6 +61,12 @@ def _load():
             lib.hjo_residual.argtypes = [i32, i64, i64, d, P, P, P]
             lib.hjo_residual_general.restype = d
             lib.hjo_residual_general.argtypes = [i32, i64, i64, P, P, P, P]
+            lib.hjo_solve_mg.restype = i32
+            lib.hjo_solve_mg.argtypes = [i32, i64, i64, d, P, P, P, i32, i64, i64, i32, i32, i32, d, i32,
+                                         i32, d, i32, d, i64, P, P, ctypes.POINTER(i64),
+                                         ctypes.POINTER(i32), ctypes.POINTER(i32)]
+            lib.hjo_mg_transfer.restype = i64
+            lib.hjo_mg_transfer.argtypes = [i32, i32, i64, i64, P, P, P, P]
             lib.hjo_resource_figures.restype = i32
             lib.hjo_resource_figures.argtypes = [i32, i64, i64, i64, i64, i64, i64, i64,
                                                  ctypes.POINTER(i64), ctypes.POINTER(i64),
@@ -118,6 +124,56 @@ def solve(dim, nx, ny, h, f, bc=None, x0=None, *, mode="hier", dtype="f64", tile
     return dict(x=x.reshape((ny, nx)) if (dim == 2 or ny > 1) else x,
                 history=None if hist is None else hist[: c + 1].copy(),
                 cycles=c, converged=bool(conv.value), status=st)
+
+
+def solve_mg(dim, nx, ny, h, f, bc=None, x0=None, *, dtype="f64", tile=(32, 32), k=4, nu1=1, nu2=1,
+             omega=None, coarse_cycles=1, levels=0, tol=1e-6, tol_mode="rel", ref_residual=0.0,
+             max_cycles=1000, history=True):
+    """Multigrid V-cycles with the hierarchical cycle as smoother (DESIGN.md
+    reading c24).  ``omega`` defaults to 4/5 (2D) and 2/3 (1D), the textbook smoothing weights
+    of damped Jacobi.  Returns dict(x, history, cycles, converged, status, levels); one cycle =
+    one V-cycle."""
+    lib = _load()
+    n = nx * ny
+    f = _f64(f, n, "f")
+    bc = _f64(bc, 2 * ny if dim == 1 else 2 * nx + 2 * ny, "bc")
+    x0 = _f64(x0, n, "x0")
+    if omega is None:
+        omega = 0.8 if dim == 2 else 2.0 / 3.0
+    x = np.zeros(n, dtype=np.float64)
+    hist = np.full(max_cycles + 1, np.nan) if history else None
+    cyc, conv, lev = ctypes.c_int64(0), ctypes.c_int(0), ctypes.c_int(0)
+    tx, ty = (tile if isinstance(tile, (tuple, list)) else (tile, 1))
+    st = lib.hjo_solve_mg(dim, nx, ny, float(h), _ptr(f), _ptr(bc), _ptr(x0), {"f64": 0, "f32": 1}[dtype],
+                          tx, ty, k, nu1, nu2, float(omega), coarse_cycles, levels, float(tol),
+                          {"rel": 0, "abs": 1}[tol_mode], float(ref_residual), int(max_cycles), _ptr(x),
+                          _ptr(hist), ctypes.byref(cyc), ctypes.byref(conv), ctypes.byref(lev))
+    if st == 2:
+        raise ValueError("oracle: invalid argument")
+    c = cyc.value
+    return dict(x=x.reshape((ny, nx)) if (dim == 2 or ny > 1) else x,
+                history=None if hist is None else hist[: c + 1].copy(),
+                cycles=c, converged=bool(conv.value), status=st, levels=lev.value)
+
+
+def mg_transfer(dim, op, nx, ny, x, a, bc=None):
+    """The multigrid transfer steps alone (double): op "restrict" -> coarse h2f = 4 R s of the fine
+    iterate x with rhs a (= h^2 f; s = a - stencil(x)); op "correct" -> x + P a for the coarse
+    interior a.  1D: ny independent problems."""
+    lib = _load()
+    x = _f64(x, nx * ny, "x")
+    bc = _f64(bc, 2 * ny if dim == 1 else 2 * nx + 2 * ny, "bc")
+    nxc, nyc = (nx - 1) // 2, ((ny - 1) // 2 if dim == 2 else ny)
+    if op == "restrict":
+        a = _f64(a, nx * ny, "a")
+        out = np.zeros(nxc * nyc)
+    else:
+        a = _f64(a, nxc * nyc, "a")
+        out = np.zeros(nx * ny)
+    w = lib.hjo_mg_transfer(dim, 0 if op == "restrict" else 1, nx, ny, _ptr(x), _ptr(bc), _ptr(a), _ptr(out))
+    if w < 0:
+        raise ValueError("oracle: invalid transfer")
+    return out
 
 
 def residual(dim, nx, ny, h, f, bc, x):

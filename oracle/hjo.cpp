@@ -18,6 +18,10 @@
 //   * stopping rule: reduce the L2 residual of the initial solution by a factor
 //     (relative test)
 //   * resource figures (shared bytes, blocks)
+//   * multigrid with the hierarchical cycle as smoother
+//                                              PAPER.md:17 (§1), :530 (§5); the textbook V-cycle
+//                                              of the tutorial the paper cites (reading c24,
+//                                              see vcycle_2d below)
 //
 // Readings where the paper is silent/garbled are SURVEY.md §8(c) c1..c18, listed
 // in DESIGN.md §3.  In particular:
@@ -119,6 +123,14 @@ inline BlockPlan block_plan(int64_t n, int64_t T, int64_t o) {
   return P;
 }
 
+// Damped (weighted) Jacobi, the multigrid smoother of SURVEY.md §8(f) NEXT #4 (reading c24):
+// x <- x + omega (u - x) with u the plain Jacobi value, evaluated as ONE fused multiply-add in T,
+// fma(omega, u - x, x).  Used only by the multigrid solver's smoothing cycles (omega != 1).
+template <typename T>
+inline T damp(T omega, T x, T u) {
+  return std::fma(omega, u - x, x);
+}
+
 // ---------------------------------------------------------------- 1D ----------
 
 // Elemental Jacobi update for -u'' = f, PAPER.md:210 (Eq. jacobi-stencil-1d-poisson):
@@ -154,6 +166,8 @@ struct Problem1D {
   std::vector<double> h2f64; // Poisson: double(h2f_i), rhs used by the residual (c16)
   std::vector<T> wl, wr;     // general: T(-a_i/d_i), T(-c_i/d_i)
   T gl, gr;                  // Dirichlet values at x=0 and x=1
+  bool weighted = false;     // multigrid smoother (reading c24): damped sub-iterations
+  T omega = T(1);
 };
 
 // x has n+2 entries: x[0] = g_left, x[1..n] interior, x[n+1] = g_right.
@@ -202,9 +216,11 @@ void hier_cycle_1d(const Problem1D<T>& p, const BlockPlan& bp, int k, int tile_o
     // Step 2: k sub-iterations on the interior; the two halo points are never
     // written (frozen at snapshot values, reading c5).
     for (int q = 0; q < k; ++q) {
-      for (int64_t i = 1; i <= w; ++i)
+      for (int64_t i = 1; i <= w; ++i) {
         B[i] = p.gen ? update1d_gen<T>(wl[i - 1], wr[i - 1], A[i - 1], A[i + 1], rhs[i - 1])
                      : update1d<T>(A[i - 1], A[i + 1], rhs[i - 1]);
+        if (p.weighted) B[i] = damp<T>(p.omega, A[i], B[i]);
+      }
       std::swap(A, B);
     }
     // Step 3: write the latest values of the OWNED points into the NEXT global array
@@ -247,6 +263,8 @@ struct Problem2D {
   T wt[4] = {T(0), T(0), T(0), T(0)};  // general: T(-a/d), T(-c/d), T(-e/d), T(-f/d)  (W, E, S, N)
   std::vector<T> h2f;        // nx*ny, row-major: Poisson T(h2*f); general q = T(b/d)
   std::vector<double> h2f64; // nx*ny, double(h2f) (c16)
+  bool weighted = false;     // multigrid smoother (reading c24): damped sub-iterations
+  T omega = T(1);
   int64_t pitch() const { return nx + 2; }
   T upd(T w, T e, T s, T n, T q) const {
     return gen ? update2d_gen<T>(wt, w, e, s, n, q) : update2d<T>(w, e, s, n, q);
@@ -307,9 +325,11 @@ void hier_cycle_2d(const Problem2D<T>& p, const BlockPlan& bx, const BlockPlan& 
     // Step 2: k sub-iterations on the interior, halo frozen.
     for (int q = 0; q < k; ++q) {
       for (int64_t jj = 1; jj <= hgt; ++jj)
-        for (int64_t ii = 1; ii <= w; ++ii)
+        for (int64_t ii = 1; ii <= w; ++ii) {
           B[jj * lp + ii] = p.upd(A[jj * lp + ii - 1], A[jj * lp + ii + 1], A[(jj - 1) * lp + ii],
                                   A[(jj + 1) * lp + ii], rhs[(jj - 1) * w + (ii - 1)]);
+          if (p.weighted) B[jj * lp + ii] = damp<T>(p.omega, A[jj * lp + ii], B[jj * lp + ii]);
+        }
       std::swap(A, B);
     }
     // Step 3: write the owned points into the next global array.
@@ -483,6 +503,275 @@ int solve2d(int64_t nx, int64_t ny, double h, const double* f, const double* bc,
   *cycles = o.cycles;
   *converged = o.converged;
   return o.status;
+}
+
+// ===================================================== multigrid (NEXT #4) ====
+// the hierarchical cycle as a multigrid smoother.  PAPER.md:17 (§1):
+// Jacobi iteration and similar stationary methods "form the backbone of highly effective
+// geometric and algebraic multigrid methods [Briggs2000]"; PAPER.md:530 (§5): the hierarchical
+// solver "has the potential to accelerate multigrid solvers which utilize this approach as a
+// smoother".  The paper gives no coarse-grid design, so reading c24 takes the
+// textbook V-cycle of the tutorial it cites (Briggs, Henson & McCormick, "A Multigrid Tutorial",
+// ch. 3-4), with the paper's hierarchical cycle as the smoother:
+//   grids     level 0 = the problem (ringed, Dirichlet data g).  Level l+1 coarsens every
+//             axis of level l that has an odd number n_l >= 3 of interior points to
+//             (n_l - 1)/2 points with spacing 2 h_l (vertex-centred and nested: coarse ringed
+//             point I is fine ringed point 2I); 2D coarsens x and y together and stops when
+//             either is even or < 3; 1D (each of the ny independent problems) coarsens x.  At
+//             most max_levels levels (0 = no limit).  Coarse rings are zero (error equation).
+//   smoother  nu1 (pre) / nu2 (post) hierarchical cycles of DAMPED Jacobi (damp(), omega) with
+//             the tile clipped to the level, k sub-iterations, halo frozen, snapshot semantics.
+//             Undamped Jacobi does not smooth (its highest mode has eigenvalue -cos(pi h)), hence
+//             the damping — the weighted Jacobi the paper's related work cites.
+//   coarsest  coarse_cycles plain (undamped) hierarchical cycles from zero.
+//   restrict  full weighting of the h^2-scaled residual s (reading c3) of the smoothed iterate.
+//             The coarse equation is A_2h e = R r with r = s / h^2, i.e. coarse
+//             h2f = (2h)^2 R r = 4 R s:
+//               2D  T(0.25 * ((4 s_C + 2 ((s_W + s_E) + (s_S + s_N))) + ((s_SW + s_SE) + (s_NW + s_NE))))
+//               1D  T(2 s_C + (s_L + s_R))
+//             (s in double, reading c16; the power-of-two factors are exact).  The coarse
+//             iterate starts at zero.
+//   correct   (bi)linear interpolation of the coarse iterate e added to the fine iterate, in T:
+//               fine on a coarse point            x + e
+//               between two coarse points         x + T(0.5)  * (e_W + e_E)   (or (e_S + e_N))
+//               between four (2D)                 x + T(0.25) * ((e_SW + e_SE) + (e_NW + e_NE))
+//   solve     one solver cycle = one V-cycle on level 0; the relative/absolute stopping test of
+//             the hierarchical solver (drive(), reading c1) after every V-cycle.
+struct MgOpts {
+  int k, nu1, nu2, coarse_cycles;
+};
+
+template <typename T>
+struct MgLevel2D {
+  Problem2D<T> p;
+  BlockPlan bx, by;
+  std::vector<T> x, y;  // iterate and the second (snapshot) array, both ringed
+};
+
+template <typename T>
+void mg_smooth_2d(MgLevel2D<T>& L, int k, int cycles, bool weighted) {
+  L.p.weighted = weighted;
+  for (int c = 0; c < cycles; ++c) {
+    hier_cycle_2d(L.p, L.bx, L.by, k, 0, L.x, L.y);
+    std::swap(L.x, L.y);
+  }
+}
+
+template <typename T>
+void mg_restrict_2d(const MgLevel2D<T>& F, MgLevel2D<T>& C) {
+  const Problem2D<T>& p = F.p;
+  const std::vector<T>& x = F.x;
+  auto s = [&](int64_t i, int64_t j) {
+    return resid2d((double)x[at(p, i, j)], (double)x[at(p, i - 1, j)], (double)x[at(p, i + 1, j)],
+                   (double)x[at(p, i, j - 1)], (double)x[at(p, i, j + 1)], p.h2f64[(j - 1) * p.nx + (i - 1)]);
+  };
+  for (int64_t J = 1; J <= C.p.ny; ++J)
+    for (int64_t I = 1; I <= C.p.nx; ++I) {
+      const int64_t i = 2 * I, j = 2 * J;
+      const double a = 4.0 * s(i, j);
+      const double b = 2.0 * ((s(i - 1, j) + s(i + 1, j)) + (s(i, j - 1) + s(i, j + 1)));
+      const double c = (s(i - 1, j - 1) + s(i + 1, j - 1)) + (s(i - 1, j + 1) + s(i + 1, j + 1));
+      const T v = (T)(0.25 * ((a + b) + c));
+      C.p.h2f[(J - 1) * C.p.nx + (I - 1)] = v;
+      C.p.h2f64[(J - 1) * C.p.nx + (I - 1)] = (double)v;
+      C.x[at(C.p, I, J)] = T(0);
+    }
+}
+
+template <typename T>
+void mg_correct_2d(MgLevel2D<T>& F, const MgLevel2D<T>& C) {
+  auto e = [&](int64_t I, int64_t J) { return C.x[at(C.p, I, J)]; };  // ring = 0
+  for (int64_t j = 1; j <= F.p.ny; ++j)
+    for (int64_t i = 1; i <= F.p.nx; ++i) {
+      const bool ci = (i % 2) == 0, cj = (j % 2) == 0;  // on a coarse line
+      T v;
+      if (ci && cj) v = e(i / 2, j / 2);
+      else if (cj) v = T(0.5) * (e((i - 1) / 2, j / 2) + e((i + 1) / 2, j / 2));
+      else if (ci) v = T(0.5) * (e(i / 2, (j - 1) / 2) + e(i / 2, (j + 1) / 2));
+      else
+        v = T(0.25) * ((e((i - 1) / 2, (j - 1) / 2) + e((i + 1) / 2, (j - 1) / 2)) +
+                       (e((i - 1) / 2, (j + 1) / 2) + e((i + 1) / 2, (j + 1) / 2)));
+      T& xv = F.x[at(F.p, i, j)];
+      xv = xv + v;
+    }
+}
+
+template <typename T>
+void vcycle_2d(std::vector<MgLevel2D<T>>& Ls, size_t l, const MgOpts& o) {
+  MgLevel2D<T>& L = Ls[l];
+  if (l + 1 == Ls.size()) {
+    mg_smooth_2d(L, o.k, o.coarse_cycles, false);
+    return;
+  }
+  mg_smooth_2d(L, o.k, o.nu1, true);
+  mg_restrict_2d(L, Ls[l + 1]);
+  vcycle_2d(Ls, l + 1, o);
+  mg_correct_2d(L, Ls[l + 1]);
+  mg_smooth_2d(L, o.k, o.nu2, true);
+}
+
+// Level sizes (reading c24): returns the interior sizes of every level.
+inline std::vector<int64_t> mg_sizes(int64_t n, int max_levels) {
+  std::vector<int64_t> v{n};
+  while ((max_levels <= 0 || (int)v.size() < max_levels) && v.back() >= 3 && (v.back() % 2) == 1)
+    v.push_back((v.back() - 1) / 2);
+  return v;
+}
+
+template <typename T>
+int solve_mg_2d(int64_t nx, int64_t ny, double h, const double* f, const double* bc, const double* x0,
+                int64_t tx, int64_t ty, const MgOpts& o, double omega, int max_levels, double tol,
+                int tol_mode, double ref_residual, int64_t max_cycles, double* x_out, double* hist,
+                int64_t* cycles, int* converged, int* levels_out) {
+  const std::vector<int64_t> sx = mg_sizes(nx, max_levels), sy = mg_sizes(ny, max_levels);
+  const size_t L = std::min(sx.size(), sy.size());
+  if (L < 2) return ST_INVALID;
+  std::vector<MgLevel2D<T>> Ls(L);
+  for (size_t l = 0; l < L; ++l) {
+    MgLevel2D<T>& V = Ls[l];
+    V.p.nx = sx[l];
+    V.p.ny = sy[l];
+    const double hl = h * (double)(int64_t(1) << l);
+    V.p.h2 = hl * hl;
+    V.p.omega = (T)omega;
+    V.p.h2f.assign(V.p.nx * V.p.ny, T(0));
+    V.p.h2f64.assign(V.p.nx * V.p.ny, 0.0);
+    V.bx = block_plan(V.p.nx, std::min<int64_t>(tx, V.p.nx), 0);
+    V.by = block_plan(V.p.ny, std::min<int64_t>(ty, V.p.ny), 0);
+    V.x.assign((V.p.nx + 2) * (V.p.ny + 2), T(0));
+  }
+  Problem2D<T>& p = Ls[0].p;
+  for (int64_t q = 0; q < nx * ny; ++q) {
+    p.h2f[q] = (T)(p.h2 * f[q]);
+    p.h2f64[q] = (double)p.h2f[q];
+  }
+  std::vector<T>& xa = Ls[0].x;
+  if (bc) {
+    for (int64_t i = 1; i <= nx; ++i) {
+      xa[at(p, i, 0)] = (T)bc[i - 1];
+      xa[at(p, i, ny + 1)] = (T)bc[nx + i - 1];
+    }
+    for (int64_t j = 1; j <= ny; ++j) {
+      xa[at(p, 0, j)] = (T)bc[2 * nx + j - 1];
+      xa[at(p, nx + 1, j)] = (T)bc[2 * nx + ny + j - 1];
+    }
+  }
+  for (auto& V : Ls) V.y = V.x;  // both arrays carry the ring
+  for (int64_t j = 1; j <= ny; ++j)
+    for (int64_t i = 1; i <= nx; ++i) xa[at(p, i, j)] = x0 ? (T)x0[(j - 1) * nx + (i - 1)] : T(0);
+  auto cycle = [&]() { vcycle_2d(Ls, 0, o); };
+  auto resid = [&]() { return residual_sq_2d(Ls[0].p, Ls[0].x); };
+  DriverOut d = drive(p.h2, tol, tol_mode, ref_residual, max_cycles, hist, cycle, resid);
+  for (int64_t j = 1; j <= ny; ++j)
+    for (int64_t i = 1; i <= nx; ++i) x_out[(j - 1) * nx + (i - 1)] = (double)Ls[0].x[at(p, i, j)];
+  *cycles = d.cycles;
+  *converged = d.converged;
+  *levels_out = (int)L;
+  return d.status;
+}
+
+template <typename T>
+struct MgLevel1D {
+  Problem1D<T> p;
+  BlockPlan bp;
+  std::vector<T> x, y;
+};
+
+template <typename T>
+void mg_smooth_1d(MgLevel1D<T>& L, int k, int cycles, bool weighted) {
+  L.p.weighted = weighted;
+  for (int c = 0; c < cycles; ++c) {
+    hier_cycle_1d(L.p, L.bp, k, 0, L.x, L.y);
+    std::swap(L.x, L.y);
+  }
+}
+
+template <typename T>
+void mg_restrict_1d(const MgLevel1D<T>& F, MgLevel1D<T>& C) {
+  const std::vector<T>& x = F.x;
+  auto s = [&](int64_t i) {
+    return resid1d((double)x[i], (double)x[i - 1], (double)x[i + 1], F.p.h2f64[i - 1]);
+  };
+  for (int64_t I = 1; I <= C.p.n; ++I) {
+    const int64_t i = 2 * I;
+    const T v = (T)(2.0 * s(i) + (s(i - 1) + s(i + 1)));
+    C.p.h2f[I - 1] = v;
+    C.p.h2f64[I - 1] = (double)v;
+    C.x[I] = T(0);
+  }
+}
+
+template <typename T>
+void mg_correct_1d(MgLevel1D<T>& F, const MgLevel1D<T>& C) {
+  for (int64_t i = 1; i <= F.p.n; ++i) {
+    const T v = (i % 2) == 0 ? C.x[i / 2] : T(0.5) * (C.x[(i - 1) / 2] + C.x[(i + 1) / 2]);
+    F.x[i] = F.x[i] + v;
+  }
+}
+
+template <typename T>
+void vcycle_1d(std::vector<MgLevel1D<T>>& Ls, size_t l, const MgOpts& o) {
+  MgLevel1D<T>& L = Ls[l];
+  if (l + 1 == Ls.size()) {
+    mg_smooth_1d(L, o.k, o.coarse_cycles, false);
+    return;
+  }
+  mg_smooth_1d(L, o.k, o.nu1, true);
+  mg_restrict_1d(L, Ls[l + 1]);
+  vcycle_1d(Ls, l + 1, o);
+  mg_correct_1d(L, Ls[l + 1]);
+  mg_smooth_1d(L, o.k, o.nu2, true);
+}
+
+// ny independent problems (the batch of NEXT #2), each with its own level hierarchy; one solver
+// cycle = one V-cycle of every problem; the stopping test uses the stacked residual.
+template <typename T>
+int solve_mg_1d(int64_t n, int64_t batch, double h, const double* f, const double* bc, const double* x0,
+                int64_t tile, const MgOpts& o, double omega, int max_levels, double tol, int tol_mode,
+                double ref_residual, int64_t max_cycles, double* x_out, double* hist, int64_t* cycles,
+                int* converged, int* levels_out) {
+  const std::vector<int64_t> sz = mg_sizes(n, max_levels);
+  const size_t L = sz.size();
+  if (L < 2) return ST_INVALID;
+  std::vector<std::vector<MgLevel1D<T>>> pb(batch, std::vector<MgLevel1D<T>>(L));
+  for (int64_t b = 0; b < batch; ++b)
+    for (size_t l = 0; l < L; ++l) {
+      MgLevel1D<T>& V = pb[b][l];
+      V.p.n = sz[l];
+      const double hl = h * (double)(int64_t(1) << l);
+      V.p.h2 = hl * hl;
+      V.p.omega = (T)omega;
+      V.p.h2f.assign(V.p.n, T(0));
+      V.p.h2f64.assign(V.p.n, 0.0);
+      V.bp = block_plan(V.p.n, std::min<int64_t>(tile, V.p.n), 0);
+      V.x.assign(V.p.n + 2, T(0));
+      if (l == 0) {
+        for (int64_t i = 0; i < n; ++i) {
+          V.p.h2f[i] = (T)(V.p.h2 * f[b * n + i]);
+          V.p.h2f64[i] = (double)V.p.h2f[i];
+        }
+        V.x[0] = bc ? (T)bc[2 * b] : T(0);
+        V.x[n + 1] = bc ? (T)bc[2 * b + 1] : T(0);
+      }
+      V.y = V.x;
+      if (l == 0)
+        for (int64_t i = 0; i < n; ++i) V.x[i + 1] = x0 ? (T)x0[b * n + i] : T(0);
+    }
+  auto cycle = [&]() {
+    for (int64_t b = 0; b < batch; ++b) vcycle_1d(pb[b], 0, o);
+  };
+  auto resid = [&]() {
+    double S = 0.0;
+    for (int64_t b = 0; b < batch; ++b) S += residual_sq_1d(pb[b][0].p, pb[b][0].x);
+    return S;
+  };
+  DriverOut d = drive(h * h, tol, tol_mode, ref_residual, max_cycles, hist, cycle, resid);
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < n; ++i) x_out[b * n + i] = (double)pb[b][0].x[i + 1];
+  *cycles = d.cycles;
+  *converged = d.converged;
+  *levels_out = (int)L;
+  return d.status;
 }
 
 }  // namespace
@@ -662,6 +951,105 @@ int hjo_resource_figures(int dim, int64_t nx, int64_t ny, int64_t tx, int64_t ty
   *threads = *tiles * tx * ty;
   *smem = bytes_per_value * (2 * (tx + 2) * (ty + 2) + tx * ty);
   return ST_OK;
+}
+
+// Multigrid with the hierarchical cycle as smoother (reading c24; see vcycle_2d / vcycle_1d).
+// Poisson only (no stencil), overlap 0.  dim 1: ny independent problems.  Returns like
+// hjo_solve; *levels_out = number of grid levels (>= 2, else ST_INVALID).
+int hjo_solve_mg(int dim, int64_t nx, int64_t ny, double h, const double* f, const double* bc,
+                 const double* x0, int dtype, int64_t tile_x, int64_t tile_y, int k, int nu1, int nu2,
+                 double omega, int coarse_cycles, int max_levels, double tol, int tol_mode,
+                 double ref_residual, int64_t max_cycles, double* x_out, double* hist, int64_t* cycles,
+                 int* converged, int* levels_out) {
+  if (!f || !x_out || !cycles || !converged || !levels_out) return ST_INVALID;
+  if (nx < 1 || ny < 1 || max_cycles < 0 || !(h > 0.0) || !std::isfinite(h)) return ST_INVALID;
+  if (k < 1 || nu1 < 0 || nu2 < 0 || nu1 + nu2 < 1 || coarse_cycles < 1) return ST_INVALID;
+  if (!(omega > 0.0) || omega > 1.0 || tile_x < 1 || (dim == 2 && tile_y < 1)) return ST_INVALID;
+  const MgOpts o{k, nu1, nu2, coarse_cycles};
+  if (dim == 1) {
+    if (dtype == 0)
+      return solve_mg_1d<double>(nx, ny, h, f, bc, x0, tile_x, o, omega, max_levels, tol, tol_mode,
+                                 ref_residual, max_cycles, x_out, hist, cycles, converged, levels_out);
+    return solve_mg_1d<float>(nx, ny, h, f, bc, x0, tile_x, o, omega, max_levels, tol, tol_mode,
+                              ref_residual, max_cycles, x_out, hist, cycles, converged, levels_out);
+  }
+  if (dim != 2) return ST_INVALID;
+  if (dtype == 0)
+    return solve_mg_2d<double>(nx, ny, h, f, bc, x0, tile_x, tile_y, o, omega, max_levels, tol, tol_mode,
+                               ref_residual, max_cycles, x_out, hist, cycles, converged, levels_out);
+  return solve_mg_2d<float>(nx, ny, h, f, bc, x0, tile_x, tile_y, o, omega, max_levels, tol, tol_mode,
+                            ref_residual, max_cycles, x_out, hist, cycles, converged, levels_out);
+}
+
+// The two grid-transfer steps alone, in double (for the pins): op 0 = restriction — coarse
+// h2f (nxc*nyc, or nxc per problem in 1D) of the fine iterate x (interior, nx*ny) with ring bc
+// (NULL = 0) and rhs h2f = h^2 f (h = 1: f itself); op 1 = correction — x + P e for the coarse
+// interior e.  Returns the number of values written to out, or -1.
+int64_t hjo_mg_transfer(int dim, int op, int64_t nx, int64_t ny, const double* x, const double* bc,
+                        const double* a, double* out) {
+  if (nx < 3 || (nx % 2) == 0 || (dim == 2 && (ny < 3 || (ny % 2) == 0)) || ny < 1) return -1;
+  const int64_t nxc = (nx - 1) / 2;
+  if (dim == 1) {
+    int64_t w = 0;
+    for (int64_t b = 0; b < ny; ++b) {
+      MgLevel1D<double> F, C;
+      F.p.n = nx;
+      F.p.h2 = 1.0;
+      F.x.assign(nx + 2, 0.0);
+      F.x[0] = bc ? bc[2 * b] : 0.0;
+      F.x[nx + 1] = bc ? bc[2 * b + 1] : 0.0;
+      for (int64_t i = 0; i < nx; ++i) F.x[i + 1] = x[b * nx + i];
+      C.p.n = nxc;
+      C.p.h2f.assign(nxc, 0.0);
+      C.p.h2f64.assign(nxc, 0.0);
+      C.x.assign(nxc + 2, 0.0);
+      if (op == 0) {
+        F.p.h2f64.assign(a + b * nx, a + (b + 1) * nx);
+        mg_restrict_1d(F, C);
+        for (int64_t I = 0; I < nxc; ++I) out[w++] = C.p.h2f64[I];
+      } else {
+        for (int64_t I = 0; I < nxc; ++I) C.x[I + 1] = a[b * nxc + I];
+        mg_correct_1d(F, C);
+        for (int64_t i = 0; i < nx; ++i) out[w++] = F.x[i + 1];
+      }
+    }
+    return w;
+  }
+  const int64_t nyc = (ny - 1) / 2;
+  MgLevel2D<double> F, C;
+  F.p.nx = nx;
+  F.p.ny = ny;
+  F.p.h2 = 1.0;
+  F.x.assign((nx + 2) * (ny + 2), 0.0);
+  if (bc) {
+    for (int64_t i = 1; i <= nx; ++i) {
+      F.x[at(F.p, i, 0)] = bc[i - 1];
+      F.x[at(F.p, i, ny + 1)] = bc[nx + i - 1];
+    }
+    for (int64_t j = 1; j <= ny; ++j) {
+      F.x[at(F.p, 0, j)] = bc[2 * nx + j - 1];
+      F.x[at(F.p, nx + 1, j)] = bc[2 * nx + ny + j - 1];
+    }
+  }
+  for (int64_t j = 1; j <= ny; ++j)
+    for (int64_t i = 1; i <= nx; ++i) F.x[at(F.p, i, j)] = x[(j - 1) * nx + (i - 1)];
+  C.p.nx = nxc;
+  C.p.ny = nyc;
+  C.p.h2f.assign(nxc * nyc, 0.0);
+  C.p.h2f64.assign(nxc * nyc, 0.0);
+  C.x.assign((nxc + 2) * (nyc + 2), 0.0);
+  if (op == 0) {
+    F.p.h2f64.assign(a, a + nx * ny);
+    mg_restrict_2d(F, C);
+    std::copy(C.p.h2f64.begin(), C.p.h2f64.end(), out);
+    return nxc * nyc;
+  }
+  for (int64_t J = 1; J <= nyc; ++J)
+    for (int64_t I = 1; I <= nxc; ++I) C.x[at(C.p, I, J)] = a[(J - 1) * nxc + (I - 1)];
+  mg_correct_2d(F, C);
+  for (int64_t j = 1; j <= ny; ++j)
+    for (int64_t i = 1; i <= nx; ++i) out[(j - 1) * nx + (i - 1)] = F.x[at(F.p, i, j)];
+  return nx * ny;
 }
 
 }  // extern "C"

@@ -246,3 +246,145 @@ def general_rhs(dim, nx, ny, stencil, b, bc):
     r[:, 0] -= a * bc[2 * nx:2 * nx + ny]
     r[:, -1] -= c * bc[2 * nx + ny:]
     return r.reshape(-1)
+
+
+# ------------------------------------------------------------------ multigrid (NEXT #4) -----
+# Dense, matrix-level constructions of the textbook V-cycle (Briggs et al., the reference of
+# PAPER.md:17) with the hierarchical damped-Jacobi smoother, written from the definitions of
+# DESIGN.md reading c24 — none of the oracle's loops.  Everything is in the h^2-scaled form:
+# level l solves K_l z = b_l (K = the 5-/3-point stencil with 4 / 2 on the diagonal, z ringed).
+
+def smoother_affine(dim, nx, ny, tx, ty, k, omega):
+    """(M, G) with x_next = M z + G b for one hierarchical cycle of DAMPED Jacobi (b = h^2 f on
+    the interior, z the ringed snapshot): per tile u <- J_w u + w (B z + D^-1 b), J_w = (1-w) I + w J."""
+    if dim == 1:
+        ny = 1
+    nz = (nx + 2) if dim == 1 else (nx + 2) * (ny + 2)
+    idx = ringed_index(nx, ny, dim)
+    dinv = 0.5 if dim == 1 else 0.25
+    interior = [(i, 0) for i in range(1, nx + 1)] if dim == 1 else \
+        [(i, j) for j in range(1, ny + 1) for i in range(1, nx + 1)]
+    pos = {p: q for q, p in enumerate(interior)}
+    n = len(interior)
+    M = np.zeros((n, nz))
+    G = np.zeros((n, n))
+    for T, owned in tiles(dim, nx, ny, tx, ty):
+        loc = {p: q for q, p in enumerate(T)}
+        w = len(T)
+        J, B, E, D = np.zeros((w, w)), np.zeros((w, nz)), np.zeros((w, nz)), np.zeros((w, n))
+        for q, (i, j) in enumerate(T):
+            E[q, idx(i, j)] = 1.0
+            D[q, pos[(i, j)]] = dinv
+            for (ii, jj) in neighbours(dim, i, j):
+                if (ii, jj) in loc:
+                    J[q, loc[(ii, jj)]] += dinv
+                else:
+                    B[q, idx(ii, jj)] += dinv
+        Jw = (1.0 - omega) * np.eye(w) + omega * J
+        S = np.zeros((w, w))
+        Jp = np.eye(w)
+        for _ in range(k):
+            S += Jp
+            Jp = Jp @ Jw
+        Mt = Jp @ E + omega * (S @ B)
+        Gt = omega * (S @ D)
+        for p in owned:
+            M[pos[p]] = Mt[loc[p]]
+            G[pos[p]] = Gt[loc[p]]
+    return M, G
+
+
+def stencil_ringed(dim, nx, ny):
+    """K (interior x ringed): (K z)_p = diag z_p - sum of the neighbours (ring included)."""
+    if dim == 1:
+        ny = 1
+    idx = ringed_index(nx, ny, dim)
+    interior = [(i, 0) for i in range(1, nx + 1)] if dim == 1 else \
+        [(i, j) for j in range(1, ny + 1) for i in range(1, nx + 1)]
+    nz = (nx + 2) if dim == 1 else (nx + 2) * (ny + 2)
+    K = np.zeros((len(interior), nz))
+    for q, (i, j) in enumerate(interior):
+        K[q, idx(i, j)] = 2.0 if dim == 1 else 4.0
+        for (ii, jj) in neighbours(dim, i, j):
+            K[q, idx(ii, jj)] -= 1.0
+    return K
+
+
+def full_weighting(dim, nx, ny):
+    """R (coarse x fine interior): 1D (1/4)[1 2 1], 2D (1/16)[1 2 1; 2 4 2; 1 2 1] centred on the
+    fine point 2I (1-based ringed), the standard full-weighting operator."""
+    nxc = (nx - 1) // 2
+    if dim == 1:
+        R = np.zeros((nxc, nx))
+        for I in range(1, nxc + 1):
+            for di, w in ((-1, 0.25), (0, 0.5), (1, 0.25)):
+                R[I - 1, 2 * I + di - 1] = w
+        return R
+    nyc = (ny - 1) // 2
+    R = np.zeros((nxc * nyc, nx * ny))
+    w1 = {-1: 0.25, 0: 0.5, 1: 0.25}
+    for J in range(1, nyc + 1):
+        for I in range(1, nxc + 1):
+            for dj in (-1, 0, 1):
+                for di in (-1, 0, 1):
+                    R[(J - 1) * nxc + I - 1, (2 * J + dj - 1) * nx + (2 * I + di - 1)] = w1[di] * w1[dj]
+    return R
+
+
+def linear_interpolation(dim, nx, ny):
+    """P (fine x coarse interior): (bi)linear interpolation with zero coarse ring; P = 2^dim R^T."""
+    return (2.0 ** dim) * full_weighting(dim, nx, ny).T
+
+
+def mg_sizes(n):
+    s = [n]
+    while s[-1] >= 3 and s[-1] % 2 == 1:
+        s.append((s[-1] - 1) // 2)
+    return s
+
+
+def vcycle_dense(dim, nx, ny, tile, k, nu1, nu2, omega, coarse_cycles):
+    """Return V(x, b, ring) -> x_next: one V-cycle on the interior x of level 0 (b = h^2 f, ring =
+    the ringed vector's ring values as a ringed array with zero interior), built from dense
+    smoother maps, K, R and P of every level."""
+    sx = mg_sizes(nx)
+    sy = mg_sizes(ny) if dim == 2 else [1] * len(sx)
+    L = min(len(sx), len(sy))
+    lev = []
+    for l in range(L):
+        n1, n2 = sx[l], sy[l]
+        t = (min(tile[0], n1), min(tile[1], n2) if dim == 2 else 1)
+        Mw, Gw = smoother_affine(dim, n1, n2, t[0], t[1], k, omega)
+        M1, G1 = smoother_affine(dim, n1, n2, t[0], t[1], k, 1.0)
+        lev.append(dict(nx=n1, ny=n2, Mw=Mw, Gw=Gw, M1=M1, G1=G1, K=stencil_ringed(dim, n1, n2)))
+    for l in range(L - 1):
+        lev[l]["R"] = full_weighting(dim, lev[l]["nx"], lev[l]["ny"])
+        lev[l]["P"] = linear_interpolation(dim, lev[l]["nx"], lev[l]["ny"])
+
+    def ringed(l, x, ring):
+        z = ring.copy()
+        d = lev[l]
+        if dim == 1:
+            z[1:-1] = x
+        else:
+            z.reshape(d["ny"] + 2, d["nx"] + 2)[1:-1, 1:-1] = x.reshape(d["ny"], d["nx"])
+        return z
+
+    def V(l, x, b, ring):
+        d = lev[l]
+        if l == L - 1:
+            for _ in range(coarse_cycles):
+                x = d["M1"] @ ringed(l, x, ring) + d["G1"] @ b
+            return x
+        for _ in range(nu1):
+            x = d["Mw"] @ ringed(l, x, ring) + d["Gw"] @ b
+        s = b - d["K"] @ ringed(l, x, ring)
+        c = lev[l + 1]
+        nzc = (c["nx"] + 2) * ((c["ny"] + 2) if dim == 2 else 1)
+        e = V(l + 1, np.zeros(c["nx"] * (c["ny"] if dim == 2 else 1)), 4.0 * (d["R"] @ s), np.zeros(nzc))
+        x = x + d["P"] @ e
+        for _ in range(nu2):
+            x = d["Mw"] @ ringed(l, x, ring) + d["Gw"] @ b
+        return x
+
+    return V, L
