@@ -68,7 +68,20 @@ typedef enum {
 } hj_status;
 
 typedef enum { HJ_F64 = 0, HJ_F32 = 1 } hj_dtype;
-typedef enum { HJ_HIERARCHICAL = 0, HJ_CLASSIC = 1 } hj_mode;
+typedef enum {
+  HJ_HIERARCHICAL = 0,  /* the paper's hierarchical cycle (§3.3, §4.1)                  */
+  HJ_CLASSIC = 1,       /* one global-memory Jacobi sweep per cycle (§3.2)              */
+  HJ_MULTIGRID = 2      /* V-cycles with the hierarchical cycle as DAMPED-Jacobi smoother
+                           (SURVEY.md §8(f) NEXT #4; PAPER.md:17, :530 name multigrid smoothing
+                           as the use of the method; reading c24 fixes the textbook
+                           V-cycle: vertex-centred coarsening n -> (n-1)/2 while n is odd >= 3
+                           (2D: both axes), full-weighting restriction of the residual, (bi)linear
+                           interpolation, mg_coarse_cycles plain hierarchical cycles on the
+                           coarsest grid).  One "cycle" = one V-cycle; the stopping test and
+                           history are those of the other modes.  Poisson only (stencil NULL),
+                           overlap 0, no row slabs; nx (and ny in 2D) odd >= 3; every level
+                           uses tile = min(tile, n_level) and k sub-iterations.               */
+} hj_mode;
 typedef enum { HJ_TOL_RELATIVE = 0, HJ_TOL_ABSOLUTE = 1 } hj_tol_mode;
 typedef enum {
   HJ_KERNEL_AUTO = 0,   /* register-resident warp-per-tile kernel where the tile shape allows
@@ -114,6 +127,13 @@ typedef struct {
   int64_t max_cycles;      /* >= 0                                                            */
   hj_kernel kernel;        /* kernel family selection (HJ_KERNEL_AUTO recommended)           */
   int32_t overlap_y;       /* 2D: overlap along y; negative = same as overlap                 */
+  /* HJ_MULTIGRID only (ignored otherwise); zeros select the defaults */
+  int32_t mg_nu1, mg_nu2;  /* pre-/post-smoothing hierarchical cycles per level, >= 0; both 0
+                              = (1, 1)                                                         */
+  double mg_omega;         /* damping of the smoothing sub-iterations, x + omega (u - x) as one
+                              fma in the iterate type, 0 < omega <= 1; 0 = 4/5 (2D), 2/3 (1D)  */
+  int32_t mg_coarse_cycles;/* plain (undamped) cycles on the coarsest grid, >= 0; 0 = 1        */
+  int32_t mg_levels;       /* maximum number of grids incl. the finest (>= 2); 0 = no limit    */
 } hj_params;
 
 typedef struct {

@@ -10,7 +10,9 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -311,7 +313,27 @@ hj_status validate(const hj_problem* pb, const hj_params* pr, bool need_f) {
   if (!pb->stencil && (!(pb->h > 0.0) || !std::isfinite(pb->h))) { set_error("h must be finite and > 0"); return HJ_ERR_INVALID_ARG; }
   if (need_f && !pb->f) { set_error("f is NULL"); return HJ_ERR_INVALID_ARG; }
   if (pb->nx > (1LL << 30) || pb->ny > (1LL << 30)) { set_error("grid too large"); return HJ_ERR_INVALID_ARG; }
-  if (pr->mode != HJ_HIERARCHICAL && pr->mode != HJ_CLASSIC) { set_error("bad mode"); return HJ_ERR_INVALID_CONFIG; }
+  if (pr->mode != HJ_HIERARCHICAL && pr->mode != HJ_CLASSIC && pr->mode != HJ_MULTIGRID) {
+    set_error("bad mode");
+    return HJ_ERR_INVALID_CONFIG;
+  }
+  if (pr->mode == HJ_MULTIGRID) {  // reading c24
+    if (pb->stencil) { set_error("multigrid: Poisson problems only (stencil must be NULL)"); return HJ_ERR_INVALID_CONFIG; }
+    if (pr->overlap != 0 || (pb->dim == 2 && pr->overlap_y > 0)) {
+      set_error("multigrid: overlap must be 0");
+      return HJ_ERR_INVALID_CONFIG;
+    }
+    if (pb->nx < 3 || (pb->nx % 2) == 0 || (pb->dim == 2 && (pb->ny < 3 || (pb->ny % 2) == 0))) {
+      set_error("multigrid: nx (and ny in 2D) must be odd and >= 3 (vertex-centred coarsening)");
+      return HJ_ERR_INVALID_CONFIG;
+    }
+    if (pb->dim == 1 && pb->ny > 65535) { set_error("multigrid: at most 65535 1D problems"); return HJ_ERR_INVALID_CONFIG; }
+    if (pr->mg_nu1 < 0 || pr->mg_nu2 < 0 || pr->mg_coarse_cycles < 0 || pr->mg_levels < 0 ||
+        pr->mg_levels == 1 || !(pr->mg_omega >= 0.0) || pr->mg_omega > 1.0) {
+      set_error("multigrid: nu1, nu2, coarse_cycles >= 0, levels 0 or >= 2, 0 <= omega <= 1");
+      return HJ_ERR_INVALID_CONFIG;
+    }
+  }
   if (pr->dtype != HJ_F64 && pr->dtype != HJ_F32) { set_error("bad dtype"); return HJ_ERR_INVALID_CONFIG; }
   if (pr->mode == HJ_HIERARCHICAL) {
     const int ox = pr->overlap, oy = pb->dim == 2 ? (pr->overlap_y < 0 ? pr->overlap : pr->overlap_y) : 0;
@@ -372,12 +394,80 @@ static hj_status choose_kernel(const hj_problem* pb, const hj_params* pr, int* k
   return HJ_OK;
 }
 
+// ------------------------------------------------------------- multigrid ---
+// Reading c24: level l+1 halves every axis of level l (n -> (n-1)/2 while n is odd >= 3; 2D both
+// axes, 1D the x axis of every independent problem), spacing 2h.  The coarse levels are internal
+// hierarchical plans (tile clipped to the level, the same k); their right-hand sides are written
+// by the restriction kernel every V-cycle, so they are built from a zero f and never reset.
+static hj_status mg_build(hj_plan* P, const hj_params* pr) {
+  const Geom& g = P->g;
+  P->mg_nu1 = pr->mg_nu1;
+  P->mg_nu2 = pr->mg_nu2;
+  if (P->mg_nu1 == 0 && P->mg_nu2 == 0) P->mg_nu1 = P->mg_nu2 = 1;
+  P->mg_coarse = pr->mg_coarse_cycles > 0 ? pr->mg_coarse_cycles : 1;
+  const double om = pr->mg_omega > 0.0 ? pr->mg_omega : (g.dim == 2 ? 0.8 : 2.0 / 3.0);
+  const double omT = g.dtype == HJ_F64 ? om : (double)(float)om;  // rounded to the iterate type
+  P->g.omega = omT;
+  std::vector<long long> sx{g.nx}, sy{g.ny};
+  auto odd3 = [](long long n) { return n >= 3 && (n % 2) == 1; };
+  while ((pr->mg_levels == 0 || (int)sx.size() < pr->mg_levels) && odd3(sx.back()) &&
+         (g.dim == 1 || odd3(sy.back()))) {
+    sx.push_back((sx.back() - 1) / 2);
+    sy.push_back(g.dim == 2 ? (sy.back() - 1) / 2 : g.ny);
+  }
+  double* zf = nullptr;
+  HJ_CUDA(cudaMalloc(&zf, sizeof(double) * size_t(sx[1]) * size_t(sy[1])));
+  hj_status s = HJ_OK;
+  cudaError_t e = cudaMemsetAsync(zf, 0, sizeof(double) * size_t(sx[1]) * size_t(sy[1]), P->stream);
+  if (e != cudaSuccess) { cudaFree(zf); set_error("multigrid setup: memset"); return HJ_ERR_CUDA; }
+  for (size_t l = 1; l < sx.size() && s == HJ_OK; ++l) {
+    hj_problem q{};
+    q.dim = g.dim;
+    q.nx = sx[l];
+    q.ny = sy[l];
+    q.h = g.h * (double)(1LL << l);
+    q.f = zf;
+    hj_params r{};
+    r.mode = HJ_HIERARCHICAL;
+    r.dtype = pr->dtype;
+    r.tile_x = (int32_t)std::min<long long>(pr->tile_x, sx[l]);
+    r.tile_y = g.dim == 2 ? (int32_t)std::min<long long>(pr->tile_y, sy[l]) : 1;
+    r.k = pr->k;
+    r.overlap = 0;
+    r.overlap_y = 0;
+    r.tol = 0.0;
+    r.tol_mode = HJ_TOL_RELATIVE;
+    r.max_cycles = 1;
+    r.kernel = pr->kernel;
+    hj_plan* C = nullptr;
+    s = plan_build(&q, &r, P->stream, nullptr, &C);
+    if (s != HJ_OK) break;
+    C->g.omega = (l + 1 == sx.size()) ? 1.0 : omT;   // coarsest: plain cycles
+    cudaFree(C->x0_d);                               // coarse levels are never reset
+    C->x0_d = nullptr;
+    P->mg.push_back(C);
+  }
+  cudaFree(zf);
+  return s;
+}
+
+static int kernels_per_smooth(const hj_plan* L) {
+  const Geom& g = L->g;
+  if (g.kernel_kind != K_REG2D) return 1;
+  const long long nfull = (g.nx / 32) * (g.ny / 32);
+  return (nfull > 0 ? 1 : 0) + (g.ntiles > nfull ? 1 : 0);
+}
+
 // ------------------------------------------------------------------ plans ---
 hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st, const DistInfo* di,
                      hj_plan** out) {
   HJ_TRY(validate(pb, pr, true));
   int nsm = 0;
   HJ_TRY(ensure_configured(&nsm));
+  if (di && pr->mode == HJ_MULTIGRID) {
+    set_error("multigrid is not supported with row slabs");
+    return HJ_ERR_INVALID_CONFIG;
+  }
   hj_plan* P = new hj_plan();
   P->prm = *pr;
   Geom& g = P->g;
@@ -581,6 +671,10 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
     s = make_tmap(&P->tmF, P->H2F, g.dtype, (u64)g.fpitch, (u64)g.frows, (u64)g.fpitch * esz, 32, 32);
     if (s != HJ_OK) return fail(s);
   }
+  if (pr->mode == HJ_MULTIGRID) {
+    s = mg_build(P, pr);
+    if (s != HJ_OK) return fail(s);
+  }
   s = plan_reset(P);
   if (s != HJ_OK) return fail(s);
 #undef PCK
@@ -616,6 +710,15 @@ hj_status plan_reset(hj_plan* P) {
 
 int launches_per_cycle(const hj_plan* P) {
   const Geom& g = P->g;
+  if (!P->mg.empty()) {  // one V-cycle (see launch_vcycle)
+    int n = (P->mg_nu1 > 0 ? P->mg_nu1 : 1) * kernels_per_smooth(P) + 2 + P->mg_nu2 * kernels_per_smooth(P) + 2;
+    for (size_t l = 0; l < P->mg.size(); ++l) {
+      const hj_plan* L = P->mg[l];
+      if (l + 1 == P->mg.size()) n += P->mg_coarse * kernels_per_smooth(L);
+      else n += (P->mg_nu1 + P->mg_nu2) * kernels_per_smooth(L) + 2;
+    }
+    return n;
+  }
   int n = 3;  // cycle kernel + rowsum + finalize
   if (g.kernel_kind == K_REG2D) {
     const long long nfull = (g.nx / 32) * (g.ny / 32);
@@ -625,8 +728,107 @@ int launches_per_cycle(const hj_plan* P) {
   return n;
 }
 
+// One hierarchical cycle of level plan L (X[in] -> X[in^1]) as a multigrid smoother; ctrl is the
+// fine plan's (done check); maxc = LLONG_MAX for the internal cycles, -1 for a residual-only pass.
+static hj_status mg_smooth(hj_plan* L, int in, long long maxc, const Ctrl* ctrl) {
+  CycleArgs a;
+  a.xin = L->X[in];
+  a.xout = L->X[in ^ 1];
+  a.h2f = L->H2F;
+  a.wl = nullptr;
+  a.wr = nullptr;
+  a.tm_in = &L->tmX[in];
+  a.tm_f = &L->tmF;
+  a.tm_out = &L->tmXs[in ^ 1];
+  a.part = L->part;
+  a.ctrl = ctrl;
+  a.max_cycles = maxc;
+  cudaError_t e = L->g.dim == 2 ? launch_cycle_2d(L->g, a, L->nsm, L->stream)
+                                : launch_cycle_1d(L->g, a, L->nsm, L->stream);
+  if (e != cudaSuccess) { set_error(std::string("smoother launch: ") + cudaGetErrorString(e)); return HJ_ERR_CUDA; }
+  return HJ_OK;
+}
+
+static hj_status mg_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) { set_error(std::string(what) + ": " + cudaGetErrorString(e)); return HJ_ERR_CUDA; }
+  return HJ_OK;
+}
+
+// Coarse level l >= 1 (P->mg[l-1]) of the V-cycle; its iterate starts at zero in X[0] (written by
+// the restriction); *out = the buffer holding its result.
+static hj_status mg_level(hj_plan* P, size_t l, int* out) {
+  hj_plan* L = P->mg[l - 1];
+  const long long INF = LLONG_MAX;
+  int cur = 0;
+  if (l == P->mg.size()) {  // coarsest grid: plain cycles from zero
+    for (int c = 0; c < P->mg_coarse; ++c, cur ^= 1) HJ_TRY(mg_smooth(L, cur, INF, P->ctrl));
+    *out = cur;
+    return HJ_OK;
+  }
+  hj_plan* N = P->mg[l];
+  for (int c = 0; c < P->mg_nu1; ++c, cur ^= 1) HJ_TRY(mg_smooth(L, cur, INF, P->ctrl));
+  HJ_TRY(mg_check(launch_mg_restrict(L->g, L->X[cur], L->H2F, N->g, N->H2F, N->X[0], P->ctrl, P->stream), "restrict"));
+  int ec = 0;
+  HJ_TRY(mg_level(P, l + 1, &ec));
+  HJ_TRY(mg_check(launch_mg_correct(L->g, L->X[cur], L->X[cur], N->g, N->X[ec], P->ctrl, P->stream), "correct"));
+  for (int c = 0; c < P->mg_nu2; ++c, cur ^= 1) HJ_TRY(mg_smooth(L, cur, INF, P->ctrl));
+  *out = cur;
+  return HJ_OK;
+}
+
+// One V-cycle of the multigrid plan: x_c in X[0] -> x_{c+1} in X[0].  The first fine smoothing
+// cycle (or a residual-only pass when nu1 = 0) carries the fused residual of x_c, reduced and
+// tested right after it, so a converged solve skips the rest of this V-cycle (every later kernel
+// checks Ctrl::done) and x_c stays intact in X[0].  The fine correction is written out of place
+// when nu1 + nu2 is odd so that every V-cycle ends in X[0].
+static hj_status launch_vcycle(hj_plan* P, bool timed) {
+  const Geom& g = P->g;
+  cudaStream_t st = P->stream;
+  const long long INF = LLONG_MAX;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timed) {
+    while (P->evpool.size() < 2 * (P->evused + 1)) {
+      cudaEvent_t ev;
+      HJ_CUDA(cudaEventCreate(&ev));
+      P->evpool.push_back(ev);
+    }
+    e0 = P->evpool[2 * P->evused];
+    e1 = P->evpool[2 * P->evused + 1];
+    P->evused++;
+    HJ_CUDA(cudaEventRecord(e0, st));
+  }
+  int cur = 0;
+  if (P->mg_nu1 > 0) {
+    HJ_TRY(mg_smooth(P, 0, P->prm.max_cycles, P->ctrl));
+    cur = 1;
+  } else {
+    HJ_TRY(mg_smooth(P, 0, -1, P->ctrl));  // residual of x_c only
+  }
+  const int wpb = 8;
+  rowsum_kernel<<<(unsigned)((g.nrg_local + wpb - 1) / wpb), 32 * wpb, 0, st>>>(
+      P->part, g.parts_per_row, g.nrg_local, g.rg_offset, P->rowsum_dst, P->ctrl, PeerDsts{}, 0);
+  HJ_CUDA(cudaGetLastError());
+  finalize_kernel<<<1, 1024, 0, st>>>(P->rowpart, g.nrg_global, P->ctrl, P->hist, P->hist_cap, g.rdiv,
+                                      P->prm.tol, (int)P->prm.tol_mode, P->prm.ref_residual,
+                                      P->prm.max_cycles, PeerSync{}, 0);
+  HJ_CUDA(cudaGetLastError());
+  for (int c = 1; c < P->mg_nu1; ++c, cur ^= 1) HJ_TRY(mg_smooth(P, cur, INF, P->ctrl));
+  hj_plan* N = P->mg[0];
+  HJ_TRY(mg_check(launch_mg_restrict(g, P->X[cur], P->H2F, N->g, N->H2F, N->X[0], P->ctrl, st), "restrict"));
+  int ec = 0;
+  HJ_TRY(mg_level(P, 1, &ec));
+  const int flip = (P->mg_nu1 + P->mg_nu2) & 1;
+  HJ_TRY(mg_check(launch_mg_correct(g, P->X[cur], P->X[cur ^ flip], N->g, N->X[ec], P->ctrl, st), "correct"));
+  cur ^= flip;
+  for (int c = 0; c < P->mg_nu2; ++c, cur ^= 1) HJ_TRY(mg_smooth(P, cur, INF, P->ctrl));
+  if (cur != 0) { set_error("internal: V-cycle parity"); return HJ_ERR_CUDA; }
+  if (timed) HJ_CUDA(cudaEventRecord(e1, st));
+  return HJ_OK;
+}
+
 // One cycle with static parity p: X[p] -> X[p^1].
 hj_status launch_cycle(hj_plan* P, int p, bool timed, float* acc_ms) {
+  if (!P->mg.empty()) return launch_vcycle(P, timed);
   const Geom& g = P->g;
   cudaStream_t st = P->stream;
   CycleArgs a;
@@ -773,7 +975,7 @@ hj_status plan_solve(hj_plan* P, hj_result* res, double* x_dev, double* hist_dev
   const Ctrl c = *P->ctrl_h;
   const long long cd = c.c_done;
   if (x_dev) {
-    const void* X = P->X[cd & 1];
+    const void* X = P->X[P->mg.empty() ? (cd & 1) : 0];  // multigrid: every V-cycle ends in X[0]
     const int blocks = 4 * P->nsm;
     if (g.dtype == HJ_F64)
       extract_kernel<double><<<blocks, 256, 0, st>>>((const double*)X, g.pitch, g.dim, g.nx, g.ny, (int)g.col0, x_dev);
@@ -794,6 +996,8 @@ hj_status plan_solve(hj_plan* P, hj_result* res, double* x_dev, double* hist_dev
 
 void plan_free(hj_plan* P) {
   if (!P) return;
+  for (hj_plan* C : P->mg) plan_free(C);
+  P->mg.clear();
   for (auto& kv : P->graphs) cudaGraphExecDestroy(kv.second);
   if (P->dist) dist_free(P);
   if (P->peer) peer_free(P);

@@ -91,6 +91,7 @@ struct Geom {
   int64_t nparts;            // number of residual partials
   int64_t nrg_local, rg_offset, nrg_global;  // row groups (tile rows) and their global offset
   double h, h2;
+  double omega = 1.0;          // damped sub-iterations (multigrid smoother, reading c24); 1 = the paper's
 };
 
 enum KernelKind { K_REG2D = 0, K_SMEM2D = 1, K_CLASSIC2D = 2, K_REG1D = 3, K_SMEM1D = 4, K_CLASSIC1D = 5 };
@@ -117,6 +118,11 @@ cudaError_t launch_cycle_1d(const Geom& g, const CycleArgs& a, int grid_hint, cu
 size_t reg1d_smem_bytes(int dtype, int tile);
 int reg1d_warps_per_cta(int dtype, int tile);
 cudaError_t reg_kernels_configure();  // opt in to large dynamic shared memory
+// Multigrid transfers (mg.cu, reading c24): gf = fine level, gc = the next coarser level.
+cudaError_t launch_mg_restrict(const Geom& gf, const void* xf, const void* qf, const Geom& gc, void* qc,
+                               void* xc, const Ctrl* ctrl, cudaStream_t st);
+cudaError_t launch_mg_correct(const Geom& gf, const void* xin, void* xout, const Geom& gc, const void* e,
+                              const Ctrl* ctrl, cudaStream_t st);
 
 // Classic kernels block geometry (CTA = 8 rows x 256 cols, one residual partial per warp).
 constexpr int CLASSIC2D_ROWS = 8;
@@ -222,6 +228,7 @@ __device__ __forceinline__ double res1(double x, double l, double r, double h2f)
 // and the Jacobi-scaled residual D^{-1}(b - Ax) = (the same chain in double) - x.
 struct Wt2 {
   double w, e, s, n;
+  double om;  // multigrid smoother damping (reading c24), T-rounded; 1 = undamped
 };
 __device__ __forceinline__ double gupd2(double ww, double we, double ws, double wn, double W,
                                         double E, double S, double N, double q) {
@@ -243,6 +250,14 @@ __device__ __forceinline__ float gupd1(float wl, float wr, float L, float R, flo
 }
 __device__ __forceinline__ double gres1(double wl, double wr, double x, double L, double R, double q) {
   return __dsub_rn(gupd1(wl, wr, L, R, q), x);
+}
+
+// Damped Jacobi (multigrid smoother, reading c24): x + omega (u - x) as ONE fma in T.
+__device__ __forceinline__ double damp(double om, double x, double u) {
+  return __fma_rn(om, __dsub_rn(u, x), x);
+}
+__device__ __forceinline__ float damp(float om, float x, float u) {
+  return __fmaf_rn(om, __fsub_rn(u, x), x);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -68,6 +68,10 @@ struct hj_plan {
   int evused = 0;
   DistState* dist = nullptr;
   PeerState* peer = nullptr;
+  // HJ_MULTIGRID (reading c24): the coarse grids 1..L-1 as internal hierarchical plans (their own
+  // buffers, Geom and omega; they share this plan's stream and Ctrl for the done check)
+  std::vector<hj_plan*> mg;
+  int mg_nu1 = 0, mg_nu2 = 0, mg_coarse = 0;
 };
 
 namespace hj {

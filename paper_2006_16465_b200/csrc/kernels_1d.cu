@@ -6,7 +6,9 @@
 // writes the interior back.  Residual of the snapshot fused: s = h2f - (2x - (L+R)).
 // GEN = true: the general tridiagonal update of Eq. 4 with per-point weights
 // wL = T(-a_i/d_i), wR = T(-c_i/d_i) stored like Q (= T(b_i/d_i)); update / residual gupd1 / gres1
-// (reading c23).
+// (reading c23).  The kernels take SK (stencil kind): 0 the paper's Poisson update,
+// 1 the general coefficients (GEN), 2 the Poisson update damped by omega (damp(): the multigrid
+// smoother of reading c24).
 #include "hj_internal.cuh"
 
 namespace hj {
@@ -42,11 +44,13 @@ struct Src1 {
   const T *x, *q, *wl, *wr;
 };
 
-template <typename T, int C, bool RAGGED, bool GEN>
+template <typename T, int C, bool RAGGED, int SK>
 __device__ __forceinline__ void reg1d_tile(const unsigned char* __restrict__ sl,
                                            T* __restrict__ xrow, long long t, int w, int lane,
                                            int kk, double* __restrict__ part, long long u,
-                                           uint64_t* bar, const Src1<T>* nxt, unsigned char* slot) {
+                                           uint64_t* bar, const Src1<T>* nxt, unsigned char* slot,
+                                           T om) {
+  constexpr bool GEN = SK == 1;
   using P = R1<T, C, GEN>;
   const T* sx = reinterpret_cast<const T*>(sl);
   const T* sf = reinterpret_cast<const T*>(sl + P::XSLOT);
@@ -113,6 +117,7 @@ __device__ __forceinline__ void reg1d_tile(const unsigned char* __restrict__ sl,
       T nv;
       if constexpr (GEN) nv = gupd1(wl[c], wr[c], prev, R, q[c]);
       else nv = upd1(prev, R, q[c]);
+      if constexpr (SK == 2) nv = damp(om, x[c], nv);
       prev = x[c];
       if (!RAGGED || ((act >> c) & 1u)) x[c] = nv;
     }
@@ -125,13 +130,15 @@ __device__ __forceinline__ void reg1d_tile(const unsigned char* __restrict__ sl,
 
 // Rows of the padded arrays are independent problems (batched 1D); tile u of the
 // launch is tile (u % ntpr) of problem (u / ntpr), and its residual partial is part[u].
-template <typename T, int C, bool GEN>
-__global__ void __launch_bounds__(R1<T, C, GEN>::WARPS * 32)
+template <typename T, int C, int SK>
+__global__ void __launch_bounds__(R1<T, C, SK == 1>::WARPS * 32)
 reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restrict__ h2f,
              const T* __restrict__ wla, const T* __restrict__ wra, int nx, long long pitch,
              long long fpitch, int ntpr, long long ntiles, double* __restrict__ part,
-             const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
+             const Ctrl* __restrict__ ctrl, int k, long long max_cycles, double omd) {
+  constexpr bool GEN = SK == 1;
   using P = R1<T, C, GEN>;
+  const T om = (T)omd;
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
   extern __shared__ unsigned char smem_raw[];
@@ -181,9 +188,9 @@ reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restric
     const Src1<T>* nxt = un < ntiles ? &nsr : nullptr;
     T* xrow = xout + (u / ntpr) * pitch;
     if (w == P::TILE)
-      reg1d_tile<T, C, false, GEN>(sl, xrow, t, w, lane, kk, part, u, &bars[s], nxt, sl);
+      reg1d_tile<T, C, false, SK>(sl, xrow, t, w, lane, kk, part, u, &bars[s], nxt, sl, om);
     else
-      reg1d_tile<T, C, true, GEN>(sl, xrow, t, w, lane, kk, part, u, &bars[s], nxt, sl);
+      reg1d_tile<T, C, true, SK>(sl, xrow, t, w, lane, kk, part, u, &bars[s], nxt, sl, om);
   }
 }
 
@@ -193,12 +200,13 @@ reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restric
 // sub-iteration, write-back of the latest container (reading c8), into the other global
 // buffer (reading c6), rhs of the updated point (reading c7).
 // =============================================================================
-template <typename T, bool GEN>
+template <typename T, int SK>
 __global__ void smem1d_kernel(const T* __restrict__ xin_all, T* __restrict__ xout_all,
                               const T* __restrict__ h2f_all, const T* __restrict__ wla,
                               const T* __restrict__ wra, int nx, long long pitch,
                               long long fpitch, Axis ax, double* __restrict__ part,
-                              const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
+                              const Ctrl* __restrict__ ctrl, int k, long long max_cycles, double omd) {
+  constexpr bool GEN = SK == 1;
   // block = (problem row, subdomain): rows of the padded arrays are independent problems
   const long long row = blockIdx.x / ax.nb;
   const T* __restrict__ xin = xin_all + row * pitch;
@@ -252,7 +260,11 @@ __global__ void smem1d_kernel(const T* __restrict__ xin_all, T* __restrict__ xou
   T* cur = A;
   T* nxt = B;
   for (int s = 0; s < kk; ++s) {
-    if (active) nxt[a + 1] = GEN ? gupd1(wl, wr, cur[a], cur[a + 2], q2) : upd1(cur[a], cur[a + 2], q2);
+    if (active) {
+      T u = GEN ? gupd1(wl, wr, cur[a], cur[a + 2], q2) : upd1(cur[a], cur[a + 2], q2);
+      if constexpr (SK == 2) u = damp((T)omd, cur[a + 1], u);  // multigrid smoother (c24)
+      nxt[a + 1] = u;
+    }
     __syncthreads();
     T* tmp = cur; cur = nxt; nxt = tmp;
   }
@@ -320,33 +332,35 @@ classic1d_kernel(const T* __restrict__ xin_all, T* __restrict__ xout_all,
   }
 }
 
-template <typename T, int C, bool GEN>
+template <typename T, int C, int SK>
 void launch_reg1d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
-  using P = R1<T, C, GEN>;
+  using P = R1<T, C, SK == 1>;
   long long ctas = (g.ntiles + P::WARPS - 1) / P::WARPS;
   if (ctas > grid_hint) ctas = grid_hint;
-  reg1d_kernel<T, C, GEN><<<(unsigned)ctas, P::WARPS * 32, P::SMEM, st>>>(
+  reg1d_kernel<T, C, SK><<<(unsigned)ctas, P::WARPS * 32, P::SMEM, st>>>(
       (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (const T*)a.wl, (const T*)a.wr, (int)g.nx,
-      g.pitch, g.fpitch, (int)g.ntx, g.ntiles, a.part, a.ctrl, g.k, a.max_cycles);
+      g.pitch, g.fpitch, (int)g.ntx, g.ntiles, a.part, a.ctrl, g.k, a.max_cycles, g.omega);
 }
 
-template <typename T, bool GEN>
+template <typename T, int SK>
 cudaError_t launch_1d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
+  constexpr bool GEN = SK == 1;
+  constexpr int SKB = GEN ? 0 : SK;  // tiles 512/1024 exist for the Poisson kinds only
   if (g.kernel_kind == K_REG1D) {
     switch (g.tx / 32) {   // GEN: tiles <= 256 (x, q, wL, wR of a lane in registers)
-      case 1: launch_reg1d<T, 1, GEN>(g, a, grid_hint * 8, st); break;
-      case 2: launch_reg1d<T, 2, GEN>(g, a, grid_hint * 8, st); break;
-      case 4: launch_reg1d<T, 4, GEN>(g, a, grid_hint * 4, st); break;
-      case 8: launch_reg1d<T, 8, GEN>(g, a, grid_hint * 4, st); break;
-      case 16: if (GEN) return cudaErrorInvalidValue; launch_reg1d<T, 16, false>(g, a, grid_hint * 2, st); break;
-      case 32: if (GEN) return cudaErrorInvalidValue; launch_reg1d<T, 32, false>(g, a, grid_hint, st); break;
+      case 1: launch_reg1d<T, 1, SK>(g, a, grid_hint * 8, st); break;
+      case 2: launch_reg1d<T, 2, SK>(g, a, grid_hint * 8, st); break;
+      case 4: launch_reg1d<T, 4, SK>(g, a, grid_hint * 4, st); break;
+      case 8: launch_reg1d<T, 8, SK>(g, a, grid_hint * 4, st); break;
+      case 16: if (GEN) return cudaErrorInvalidValue; launch_reg1d<T, 16, SKB>(g, a, grid_hint * 2, st); break;
+      case 32: if (GEN) return cudaErrorInvalidValue; launch_reg1d<T, 32, SKB>(g, a, grid_hint, st); break;
       default: return cudaErrorInvalidValue;
     }
   } else if (g.kernel_kind == K_SMEM1D) {
     const size_t smem = sizeof(T) * (2 * size_t(g.tx + 2) + size_t(g.tx));
-    smem1d_kernel<T, GEN><<<(unsigned)g.ntiles, g.tx, smem, st>>>(
+    smem1d_kernel<T, SK><<<(unsigned)g.ntiles, g.tx, smem, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (const T*)a.wl, (const T*)a.wr, (int)g.nx,
-        g.pitch, g.fpitch, g.ax, a.part, a.ctrl, g.k, a.max_cycles);
+        g.pitch, g.fpitch, g.ax, a.part, a.ctrl, g.k, a.max_cycles, g.omega);
   } else {
     classic1d_kernel<T, GEN><<<(unsigned)g.ntiles, 256, 0, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, (const T*)a.wl, (const T*)a.wr, (int)g.nx,
@@ -355,10 +369,10 @@ cudaError_t launch_1d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
   return cudaGetLastError();
 }
 
-template <typename T, int C, bool GEN = false>
+template <typename T, int C, int SK = 0>
 cudaError_t cfg1() {
-  return cudaFuncSetAttribute(reg1d_kernel<T, C, GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)R1<T, C, GEN>::SMEM);
+  return cudaFuncSetAttribute(reg1d_kernel<T, C, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)R1<T, C, SK == 1>::SMEM);
 }
 
 }  // namespace
@@ -375,8 +389,11 @@ cudaError_t configure_1d() {
   if ((e = cfg1<T, 1>()) != cudaSuccess || (e = cfg1<T, 2>()) != cudaSuccess ||                \
       (e = cfg1<T, 4>()) != cudaSuccess || (e = cfg1<T, 8>()) != cudaSuccess ||                \
       (e = cfg1<T, 16>()) != cudaSuccess || (e = cfg1<T, 32>()) != cudaSuccess ||              \
-      (e = cfg1<T, 1, true>()) != cudaSuccess || (e = cfg1<T, 2, true>()) != cudaSuccess ||    \
-      (e = cfg1<T, 4, true>()) != cudaSuccess || (e = cfg1<T, 8, true>()) != cudaSuccess)      \
+      (e = cfg1<T, 1, 1>()) != cudaSuccess || (e = cfg1<T, 2, 1>()) != cudaSuccess ||          \
+      (e = cfg1<T, 4, 1>()) != cudaSuccess || (e = cfg1<T, 8, 1>()) != cudaSuccess ||          \
+      (e = cfg1<T, 1, 2>()) != cudaSuccess || (e = cfg1<T, 2, 2>()) != cudaSuccess ||          \
+      (e = cfg1<T, 4, 2>()) != cudaSuccess || (e = cfg1<T, 8, 2>()) != cudaSuccess ||          \
+      (e = cfg1<T, 16, 2>()) != cudaSuccess || (e = cfg1<T, 32, 2>()) != cudaSuccess)          \
     return e;
   HJ_CFG(double)
   HJ_CFG(float)
@@ -386,10 +403,13 @@ cudaError_t configure_1d() {
 
 cudaError_t launch_cycle_1d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
   if (g.gen)
-    return g.dtype == HJ_F64 ? launch_1d_t<double, true>(g, a, grid_hint, st)
-                             : launch_1d_t<float, true>(g, a, grid_hint, st);
-  return g.dtype == HJ_F64 ? launch_1d_t<double, false>(g, a, grid_hint, st)
-                           : launch_1d_t<float, false>(g, a, grid_hint, st);
+    return g.dtype == HJ_F64 ? launch_1d_t<double, 1>(g, a, grid_hint, st)
+                             : launch_1d_t<float, 1>(g, a, grid_hint, st);
+  if (g.omega != 1.0)  // damped sub-iterations: the multigrid smoother (reading c24)
+    return g.dtype == HJ_F64 ? launch_1d_t<double, 2>(g, a, grid_hint, st)
+                             : launch_1d_t<float, 2>(g, a, grid_hint, st);
+  return g.dtype == HJ_F64 ? launch_1d_t<double, 0>(g, a, grid_hint, st)
+                           : launch_1d_t<float, 0>(g, a, grid_hint, st);
 }
 
 }  // namespace hj

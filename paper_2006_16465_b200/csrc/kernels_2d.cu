@@ -5,9 +5,11 @@
 // and copies the interior back.  PAPER.md:114-133 (§3.2): the classic sweep.
 // Every kernel also reduces the h^2-scaled residual of the snapshot it reads:
 // s = h2f - (4x - ((W+E)+(S+N))), sum of s^2 per tile -> part[tile].
-// GEN = true: the general constant-coefficient stencil of Eq. 10 — the update
-// and residual of hj_internal.cuh gupd2 / gres2 (reading c23) with the weights held as
-// kernel parameters; everything else (tiles, halo, stores) is unchanged.
+// SK (stencil kind) = 1: the general constant-coefficient stencil of Eq. 10 —
+// the update and residual of hj_internal.cuh gupd2 / gres2 (reading c23) with the
+// weights held as kernel parameters; SK = 2: the Poisson update damped by omega (damp(), the
+// multigrid smoother of reading c24); SK = 0: the paper's Poisson update.  Everything else (tiles,
+// halo, stores) is unchanged.
 #include <type_traits>
 
 #include "hj_internal.cuh"
@@ -51,11 +53,14 @@ struct R2 {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <typename T, bool MASK, bool GEN>
+template <typename T, bool MASK, int SK>
 struct Tile2 {
+  static constexpr bool GEN = SK == 1;  // general coefficients (Eq. 10, reading c23)
+  static constexpr bool WGT = SK == 2;  // damped Jacobi: the multigrid smoother (reading c24)
   T x[8][4];      // current iterate
   T q[8][4];      // 0.25 * h^2 f  (GEN: b / d)
   T cw[4];        // GEN: weights W, E, S, N
+  T om;           // WGT: damping factor omega
   const T* hxp;   // per-warp smem: frozen W (lx == 0) / E (lx == 7) halo of my 8 rows
   const T* hyp;   // per-warp smem: frozen S (ly == 0) / N (ly == 3) halo of my 4 columns
   uint32_t own;   // MASK (overlapping blocks): bit 4*i+c set if this block owns cell (i, c)
@@ -150,11 +155,13 @@ struct Tile2 {
         } else if constexpr (RES) {
           const double sum = __dadd_rn(__dadd_rn(W, E), __dadd_rn(S, N));
           nw[c] = __fma_rn(0.25, sum, q[i][c]);
+          if constexpr (WGT) nw[c] = damp(om, x[i][c], nw[c]);
           const double t = __fma_rn(4.0, x[i][c], -sum);
           const double r = __fma_rn(4.0, q[i][c], -t);
           if (on(i, c)) acc[c] = __fma_rn(r, r, acc[c]);
         } else {
           nw[c] = upd(W, E, S, N, q[i][c]);
+          if constexpr (WGT) nw[c] = damp(om, x[i][c], nw[c]);
         }
       }
 #pragma unroll
@@ -170,7 +177,7 @@ struct Tile2 {
 };
 
 // One full 32x32 tile: smem slot -> registers, refill, fused residual, k sub-iterations, store.
-template <typename T, typename C, bool MASK, bool GEN, typename Refill, typename Store>
+template <typename T, typename C, bool MASK, int SK, typename Refill, typename Store>
 __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ sx, const T* __restrict__ sf,
                                            T* __restrict__ so, T* __restrict__ hb, int lane, int kk,
                                            double* __restrict__ part, long long t, Refill&& refill,
@@ -178,10 +185,11 @@ __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ 
                                            int ox0, int ox1, int oy0, int oy1) {
   using V2 = typename VecOf<T>::v2;
   const int lx = lane & 7, ly = lane >> 3;
-  Tile2<T, MASK, GEN> tl;
-  if constexpr (GEN) {
+  Tile2<T, MASK, SK> tl;
+  if constexpr (SK == 1) {
     tl.cw[0] = (T)wt.w; tl.cw[1] = (T)wt.e; tl.cw[2] = (T)wt.s; tl.cw[3] = (T)wt.n;
   }
+  if constexpr (SK == 2) tl.om = (T)wt.om;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {  // 128-bit shared loads
     const int r = 8 * ly + i;
@@ -270,7 +278,7 @@ __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ 
 // Persistent kernel over the FULL 32x32 tiles (ntx_full x nty_full of them; ragged edge tiles,
 // if any, are done by smem2d_kernel in edge mode).  Warp w handles full tiles w, w+W, ...;
 // partials are indexed by the global tile index ty*ntx + tx.
-template <typename T, typename C, bool MASK, bool GEN>
+template <typename T, typename C, bool MASK, int SK>
 __global__ void __launch_bounds__(C::WARPS * 32, 1)
 reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
              const __grid_constant__ CUtensorMap tmO, T* __restrict__ xout, long long pitch,
@@ -311,7 +319,7 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
     mbar_wait(bar, it & 1);
     const int tx = (int)(u % ntx_full), ty = (int)(u / ntx_full);
     const int x0 = axis_start(ax, tx), y0 = axis_start(ay, ty);
-    reg2d_tile<T, C, MASK, GEN>(
+    reg2d_tile<T, C, MASK, SK>(
         wt, sx, sf, so, hb, lane, kk, part, (long long)ty * ntx + tx,
         [&] {
           if (lane == 0 && u + nw < nfull) {
@@ -339,11 +347,12 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
 // =============================================================================
 // edge != 0: only the ragged edge tiles — blocks [0, nty) are the last tile column (if nx is
 // ragged), the following blocks the last tile row (if ny is ragged) — for REG2D grids.
-template <typename T, bool GEN>
+template <typename T, int SK>
 __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
                               const T* __restrict__ h2f, long long pitch, long long fpitch, int nx,
                               int ny, Axis ax, Axis ay, int edge, double* __restrict__ part,
                               const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt) {
+  constexpr bool GEN = SK == 1;  // general coefficients (reading c23)
   const int ntx = ax.nb, nty = ay.nb;
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
@@ -409,9 +418,12 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
   T* cur = A;
   T* nxt = B;
   for (int s = 0; s < kk; ++s) {
-    if (active)
-      nxt[c] = GEN ? gupd2(ww, we, ws, wn, cur[c - 1], cur[c + 1], cur[c - L], cur[c + L], q4)
-                   : upd2(cur[c - 1], cur[c + 1], cur[c - L], cur[c + L], q4);
+    if (active) {
+      T u = GEN ? gupd2(ww, we, ws, wn, cur[c - 1], cur[c + 1], cur[c - L], cur[c + L], q4)
+                : upd2(cur[c - 1], cur[c + 1], cur[c - L], cur[c + L], q4);
+      if constexpr (SK == 2) u = damp((T)wt.om, cur[c], u);  // multigrid smoother (c24)
+      nxt[c] = u;
+    }
     __syncthreads();
     T* tmp = cur; cur = nxt; nxt = tmp;
   }
@@ -515,9 +527,9 @@ classic2d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __res
   if (lane == 0) part[(rb * ncb + cb) * 4 + warp] = acc;
 }
 
-template <typename T, bool GEN>
+template <typename T, int SK>
 cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
-  const Wt2 wt{g.wt[0], g.wt[1], g.wt[2], g.wt[3]};
+  const Wt2 wt{g.wt[0], g.wt[1], g.wt[2], g.wt[3], g.omega};
   const size_t smem_paper = sizeof(T) * (2 * size_t(g.tx + 2) * (g.ty + 2) + size_t(g.tx) * g.ty);
   if (g.kernel_kind == K_REG2D) {
     // o = 0: the full 32x32 tiles here, ragged edge tiles by smem2d in edge mode;
@@ -530,7 +542,7 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
         using C = decltype(cfg);
         long long ctas = (nfull + C::WARPS - 1) / C::WARPS;
         if (ctas > grid_hint) ctas = grid_hint;
-        reg2d_kernel<T, C, decltype(mask)::value, GEN><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
+        reg2d_kernel<T, C, decltype(mask)::value, SK><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
             *a.tm_in, *a.tm_f, *a.tm_out, (T*)a.xout, g.pitch, g.ax, g.ay, (int)ntx_full, nfull,
             (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles, wt);
       };
@@ -539,15 +551,15 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
     }
     const long long nedge = g.ntiles - nfull;
     if (nedge > 0)
-      smem2d_kernel<T, GEN><<<(unsigned)nedge, dim3(32, 32), smem_paper, st>>>(
+      smem2d_kernel<T, SK><<<(unsigned)nedge, dim3(32, 32), smem_paper, st>>>(
           (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
           g.ax, g.ay, 1, a.part, a.ctrl, g.k, a.max_cycles, wt);
   } else if (g.kernel_kind == K_SMEM2D) {
-    smem2d_kernel<T, GEN><<<(unsigned)g.ntiles, dim3(g.tx, g.ty), smem_paper, st>>>(
+    smem2d_kernel<T, SK><<<(unsigned)g.ntiles, dim3(g.tx, g.ty), smem_paper, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
         g.ax, g.ay, 0, a.part, a.ctrl, g.k, a.max_cycles, wt);
   } else {
-    classic2d_kernel<T, GEN><<<(unsigned)(g.ntx * g.nty), 128, 0, st>>>(
+    classic2d_kernel<T, SK == 1><<<(unsigned)(g.ntx * g.nty), 128, 0, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
         (int)g.ntx, a.part, a.ctrl, a.max_cycles, wt);
   }
@@ -557,31 +569,36 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
 }  // namespace
 
 
-template <typename T, typename C, bool GEN>
+template <typename T, typename C, int SK>
 cudaError_t cfg2() {
-  cudaError_t e = cudaFuncSetAttribute(reg2d_kernel<T, C, false, GEN>,
+  cudaError_t e = cudaFuncSetAttribute(reg2d_kernel<T, C, false, SK>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(reg2d_kernel<T, C, true, GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(reg2d_kernel<T, C, true, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)C::SMEM);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(smem2d_kernel<T, GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  return cudaFuncSetAttribute(smem2d_kernel<T, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
 cudaError_t configure_2d() {
   cudaError_t e;
-  if ((e = cfg2<double, R2<double>, false>()) != cudaSuccess) return e;
-  if ((e = cfg2<float, R2<float>, false>()) != cudaSuccess) return e;
-  if ((e = cfg2<double, R2<double>, true>()) != cudaSuccess) return e;
-  return cfg2<float, R2<float>, true>();
+  if ((e = cfg2<double, R2<double>, 0>()) != cudaSuccess) return e;
+  if ((e = cfg2<float, R2<float>, 0>()) != cudaSuccess) return e;
+  if ((e = cfg2<double, R2<double>, 1>()) != cudaSuccess) return e;
+  if ((e = cfg2<float, R2<float>, 1>()) != cudaSuccess) return e;
+  if ((e = cfg2<double, R2<double>, 2>()) != cudaSuccess) return e;
+  return cfg2<float, R2<float>, 2>();
 }
 
 cudaError_t launch_cycle_2d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
   if (g.gen)
-    return g.dtype == HJ_F64 ? launch_2d_t<double, true>(g, a, grid_hint, st)
-                             : launch_2d_t<float, true>(g, a, grid_hint, st);
-  return g.dtype == HJ_F64 ? launch_2d_t<double, false>(g, a, grid_hint, st)
-                           : launch_2d_t<float, false>(g, a, grid_hint, st);
+    return g.dtype == HJ_F64 ? launch_2d_t<double, 1>(g, a, grid_hint, st)
+                             : launch_2d_t<float, 1>(g, a, grid_hint, st);
+  if (g.omega != 1.0)  // damped sub-iterations: the multigrid smoother (reading c24)
+    return g.dtype == HJ_F64 ? launch_2d_t<double, 2>(g, a, grid_hint, st)
+                             : launch_2d_t<float, 2>(g, a, grid_hint, st);
+  return g.dtype == HJ_F64 ? launch_2d_t<double, 0>(g, a, grid_hint, st)
+                           : launch_2d_t<float, 0>(g, a, grid_hint, st);
 }
 
 }  // namespace hj

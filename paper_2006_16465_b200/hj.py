@@ -20,7 +20,7 @@ HJ_OK, HJ_NOT_CONVERGED, HJ_ERR_INVALID_ARG, HJ_ERR_INVALID_CONFIG = 0, 1, 2, 3
 HJ_ERR_NUMERIC, HJ_ERR_CUDA, HJ_ERR_NCCL, HJ_ERR_OOM = 4, 5, 6, 7
 STATUS_NAMES = {0: "HJ_OK", 1: "HJ_NOT_CONVERGED", 2: "HJ_ERR_INVALID_ARG", 3: "HJ_ERR_INVALID_CONFIG",
                 4: "HJ_ERR_NUMERIC", 5: "HJ_ERR_CUDA", 6: "HJ_ERR_NCCL", 7: "HJ_ERR_OOM"}
-MODES = {"hier": 0, "hierarchical": 0, "classic": 1}
+MODES = {"hier": 0, "hierarchical": 0, "classic": 1, "mg": 2, "multigrid": 2}
 DTYPES = {"f64": 0, "float64": 0, "f32": 1, "float32": 1}
 TOL_MODES = {"rel": 0, "relative": 0, "abs": 1, "absolute": 1}
 KERNELS = {"auto": 0, "smem": 1}
@@ -42,7 +42,9 @@ class hj_params(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int), ("dtype", ctypes.c_int), ("tile_x", ctypes.c_int32),
                 ("tile_y", ctypes.c_int32), ("k", ctypes.c_int32), ("overlap", ctypes.c_int32),
                 ("tol", ctypes.c_double), ("tol_mode", ctypes.c_int), ("ref_residual", ctypes.c_double),
-                ("max_cycles", ctypes.c_int64), ("kernel", ctypes.c_int), ("overlap_y", ctypes.c_int32)]
+                ("max_cycles", ctypes.c_int64), ("kernel", ctypes.c_int), ("overlap_y", ctypes.c_int32),
+                ("mg_nu1", ctypes.c_int32), ("mg_nu2", ctypes.c_int32), ("mg_omega", ctypes.c_double),
+                ("mg_coarse_cycles", ctypes.c_int32), ("mg_levels", ctypes.c_int32)]
 
 
 class hj_result(ctypes.Structure):
@@ -121,13 +123,17 @@ def _check(st, ok=(HJ_OK, HJ_NOT_CONVERGED)):
 
 
 def make_params(mode="hier", dtype="f64", tile=(32, 32), k=None, overlap=0, tol=1e-4, tol_mode="rel",
-                ref_residual=0.0, max_cycles=10**6, kernel="auto"):
+                ref_residual=0.0, max_cycles=10**6, kernel="auto", nu1=0, nu2=0, omega=0.0,
+                coarse_cycles=0, levels=0):
+    """hj_params.  mode "mg": multigrid V-cycles (nu1/nu2 smoothing cycles, damping omega,
+    coarse_cycles on the coarsest grid, at most `levels` grids; zeros = the library defaults)."""
     tx, ty = tile if isinstance(tile, (tuple, list)) else (tile, 1)
     if k is None:
-        k = 1 if MODES[mode] == 1 else 16
+        k = 1 if MODES[mode] == 1 else (4 if MODES[mode] == 2 else 16)
     ox, oy = overlap if isinstance(overlap, (tuple, list)) else (overlap, -1)
     return hj_params(MODES[mode], DTYPES[dtype], tx, ty, k, ox,
-                     float(tol), TOL_MODES[tol_mode], float(ref_residual), int(max_cycles), KERNELS[kernel], oy)
+                     float(tol), TOL_MODES[tol_mode], float(ref_residual), int(max_cycles), KERNELS[kernel], oy,
+                     int(nu1), int(nu2), float(omega), int(coarse_cycles), int(levels))
 
 
 def _host(a, n, name):

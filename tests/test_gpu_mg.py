@@ -1,0 +1,106 @@
+"""GPU parity of the multigrid solver (reading c24).
+
+The CUDA V-cycle (damped hierarchical smoothing kernels, restriction and correction kernels, the
+engine's level recursion) against the oracle's V-cycle on the same seeded inputs: iterates
+bitwise after 1, 2 and 5 V-cycles (f64 and f32), residual history within 1e-12 relative, V-cycle
+counts to tolerance exactly equal.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2006_16465_b200 import hj
+from paper_2006_16465_b200.inputs import make_problem
+
+pytestmark = pytest.mark.gpu
+
+
+def both(p, *, cycles, tol=0.0, **prm):
+    kw = dict(prm)
+    oracle_kw = {k: v for k, v in kw.items() if k != "kernel"}
+    o = oracle.solve_mg(p["dim"], p["nx"], p["ny"], p["h"], p["f"], p["bc"], p["x0"], tol=tol,
+                        max_cycles=cycles, **oracle_kw)
+    g = hj.jacobi_solve(p["dim"], p["nx"], p["ny"], p["h"], p["f"], p["bc"], p["x0"], mode="mg", tol=tol,
+                        max_cycles=cycles, **kw)
+    return o, g
+
+
+def assert_parity(o, g):
+    assert g["cycles"] == o["cycles"]
+    bad = np.argwhere(g["x"] != o["x"])
+    assert bad.size == 0, f"{len(bad)} mismatching cells, first {bad[:5].tolist()}"
+    np.testing.assert_allclose(g["history"], o["history"], rtol=1e-12, atol=0)
+
+
+CASES_2D = [  # (nx, ny, tile, k, nu1, nu2, omega, coarse, levels, kernel)
+    (63, 63, (32, 32), 4, 1, 1, 0.8, 1, 0, "auto"),
+    (127, 95, (32, 32), 3, 2, 1, 0.7, 2, 0, "auto"),      # ragged tiles on every level, odd nu1+nu2
+    (65, 33, (32, 32), 2, 0, 1, 0.6, 3, 0, "auto"),       # nu1 = 0: residual-only pass
+    (31, 31, (8, 4), 5, 1, 2, 0.8, 4, 0, "auto"),          # smem kernel on every level
+    (127, 127, (32, 32), 4, 1, 1, 0.8, 8, 3, "auto"),      # 3 levels, 31x31 coarsest
+    (63, 63, (16, 16), 3, 1, 1, 0.8, 1, 0, "smem"),
+]
+
+
+@pytest.mark.parametrize("proto", ["R", "P"])
+@pytest.mark.parametrize("nx,ny,tile,k,nu1,nu2,omega,cc,lv,kernel", CASES_2D)
+@pytest.mark.parametrize("cycles", [1, 2, 5])
+def test_mg2d_bitwise(nx, ny, tile, k, nu1, nu2, omega, cc, lv, kernel, cycles, proto):
+    p = make_problem(proto, 2, nx, ny)
+    o, g = both(p, cycles=cycles, tile=tile, k=k, nu1=nu1, nu2=nu2, omega=omega, coarse_cycles=cc,
+                levels=lv, kernel=kernel)
+    assert_parity(o, g)
+
+
+@pytest.mark.parametrize("nx,ny,tile,k", [(127, 95, (32, 32), 3), (63, 63, (8, 8), 4)])
+def test_mg2d_f32_bitwise(nx, ny, tile, k):
+    p = make_problem("R", 2, nx, ny)
+    o, g = both(p, cycles=4, tile=tile, k=k, dtype="f32")
+    assert_parity(o, g)
+
+
+@pytest.mark.parametrize("n,batch,tile,k,nu1,nu2", [(255, 1, 32, 4, 1, 1), (1023, 3, 64, 3, 2, 1),
+                                                    (127, 4, 20, 5, 1, 2), (2047, 2, 1024, 2, 1, 1)])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_mg1d_bitwise(n, batch, tile, k, nu1, nu2, dtype):
+    p = make_problem("R", 1, n, batch=batch)
+    o, g = both(p, cycles=3, tile=tile, k=k, nu1=nu1, nu2=nu2, dtype=dtype)
+    assert_parity(o, g)
+
+
+@pytest.mark.parametrize("dim,n,proto,tol", [(2, 255, "P", 1e-10), (2, 127, "M", 1e-8), (1, 4095, "P", 1e-10)])
+def test_mg_counts_to_tolerance(dim, n, proto, tol):
+    p = make_problem(proto, dim, n)
+    o, g = both(p, cycles=200, tol=tol, tile=(32, 32) if dim == 2 else 256, k=4)
+    assert o["converged"] and g["converged"]
+    assert_parity(o, g)
+
+
+def test_mg_plan_resume_and_launch_count():
+    import torch
+    n = 255
+    p = make_problem("R", 2, n)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.as_tensor(a, device=dev)
+    plan = hj.Plan(2, n, n, p["h"], t(p["f"]), t(p["bc"]), t(p["x0"]), mode="mg", tile=(32, 32), k=4,
+                   tol=0.0, max_cycles=6)
+    assert plan.launches_per_cycle() > 10
+    plan.run(3)
+    r = plan.solve()
+    o = oracle.solve_mg(2, n, n, p["h"], p["f"], p["bc"], p["x0"], tile=(32, 32), k=4, tol=0.0, max_cycles=6)
+    assert r["cycles"] == 6
+    assert np.array_equal(r["x"].cpu().numpy(), o["x"])
+    plan.close()
+
+
+def test_mg_invalid_configs():
+    p = make_problem("P", 2, 64)
+    for kw in (dict(), dict(overlap=2)):
+        with pytest.raises(hj.HJError) as e:
+            hj.jacobi_solve(2, 64, 64, p["h"], p["f"], None, None, mode="mg", **kw)
+        assert e.value.status == hj.HJ_ERR_INVALID_CONFIG
+    q = make_problem("P", 2, 63)
+    with pytest.raises(hj.HJError):
+        hj.jacobi_solve(2, 63, 63, q["h"], q["f"], None, None, mode="mg", omega=1.5)
+    with pytest.raises(hj.HJError):
+        hj.jacobi_solve(2, 63, 63, q["h"], q["f"], None, None, mode="mg", levels=1)
