@@ -443,6 +443,12 @@ static hj_status mg_build(hj_plan* P, const hj_params* pr) {
     s = plan_build(&q, &r, P->stream, nullptr, &C);
     if (s != HJ_OK) break;
     C->g.omega = (l + 1 == sx.size()) ? 1.0 : omT;   // coarsest: plain cycles
+    if (g.dim == 2) {  // TMA boxes of the coarse patch under a fine 32x32 tile + halo (fused correction)
+      const size_t esz = g.dtype == HJ_F64 ? 8 : 4;
+      for (int b = 0; b < 2 && s == HJ_OK; ++b)
+        s = make_tmap(&C->tmE[b], C->X[b], C->g.dtype, (uint64_t)C->g.pitch, (uint64_t)C->g.rows,
+                      (uint64_t)C->g.pitch * esz, esz == 8 ? 20 : 24, 18);  // R2<T>::EW x EH
+    }
     cudaFree(C->x0_d);                               // coarse levels are never reset
     C->x0_d = nullptr;
     P->mg.push_back(C);
@@ -710,12 +716,16 @@ hj_status plan_reset(hj_plan* P) {
 
 int launches_per_cycle(const hj_plan* P) {
   const Geom& g = P->g;
-  if (!P->mg.empty()) {  // one V-cycle (see launch_vcycle)
-    int n = (P->mg_nu1 > 0 ? P->mg_nu1 : 1) * kernels_per_smooth(P) + 2 + P->mg_nu2 * kernels_per_smooth(P) + 2;
+  if (!P->mg.empty()) {  // one V-cycle (see launch_vcycle): smoothing, rowsum + finalize,
+                         // restriction, correction (unless fused into the post-smoothing)
+    const bool fuse2d = g.dim == 2 && P->mg_nu2 > 0;
+    const bool fine_fused = fuse2d && ((P->mg_nu1 + P->mg_nu2) & 1) == 0;
+    int n = (P->mg_nu1 > 0 ? P->mg_nu1 : 1) * kernels_per_smooth(P) + 2 + P->mg_nu2 * kernels_per_smooth(P) +
+            1 + (fine_fused ? 0 : 1);
     for (size_t l = 0; l < P->mg.size(); ++l) {
       const hj_plan* L = P->mg[l];
       if (l + 1 == P->mg.size()) n += P->mg_coarse * kernels_per_smooth(L);
-      else n += (P->mg_nu1 + P->mg_nu2) * kernels_per_smooth(L) + 2;
+      else n += (P->mg_nu1 + P->mg_nu2) * kernels_per_smooth(L) + 1 + (fuse2d ? 0 : 1);
     }
     return n;
   }
@@ -730,8 +740,14 @@ int launches_per_cycle(const hj_plan* P) {
 
 // One hierarchical cycle of level plan L (X[in] -> X[in^1]) as a multigrid smoother; ctrl is the
 // fine plan's (done check); maxc = LLONG_MAX for the internal cycles, -1 for a residual-only pass.
-static hj_status mg_smooth(hj_plan* L, int in, long long maxc, const Ctrl* ctrl) {
+static hj_status mg_smooth(hj_plan* L, int in, long long maxc, const Ctrl* ctrl,
+                           const hj_plan* cor = nullptr, int cor_buf = 0) {
   CycleArgs a;
+  if (cor) {  // fused coarse-grid correction (2D): the snapshot is x + P e, e = cor->X[cor_buf]
+    a.cor_e = cor->X[cor_buf];
+    a.cor_pitch = cor->g.pitch;
+    a.tm_cor = &cor->tmE[cor_buf];
+  }
   a.xin = L->X[in];
   a.xout = L->X[in ^ 1];
   a.h2f = L->H2F;
@@ -770,8 +786,15 @@ static hj_status mg_level(hj_plan* P, size_t l, int* out) {
   HJ_TRY(mg_check(launch_mg_restrict(L->g, L->X[cur], L->H2F, N->g, N->H2F, N->X[0], P->ctrl, P->stream), "restrict"));
   int ec = 0;
   HJ_TRY(mg_level(P, l + 1, &ec));
-  HJ_TRY(mg_check(launch_mg_correct(L->g, L->X[cur], L->X[cur], N->g, N->X[ec], P->ctrl, P->stream), "correct"));
-  for (int c = 0; c < P->mg_nu2; ++c, cur ^= 1) HJ_TRY(mg_smooth(L, cur, INF, P->ctrl));
+  int c = 0;
+  if (L->g.dim == 2 && P->mg_nu2 > 0) {  // correction fused into the first post-smoothing cycle
+    HJ_TRY(mg_smooth(L, cur, INF, P->ctrl, N, ec));
+    cur ^= 1;
+    c = 1;
+  } else {
+    HJ_TRY(mg_check(launch_mg_correct(L->g, L->X[cur], L->X[cur], N->g, N->X[ec], P->ctrl, P->stream), "correct"));
+  }
+  for (; c < P->mg_nu2; ++c, cur ^= 1) HJ_TRY(mg_smooth(L, cur, INF, P->ctrl));
   *out = cur;
   return HJ_OK;
 }
@@ -818,9 +841,16 @@ static hj_status launch_vcycle(hj_plan* P, bool timed) {
   int ec = 0;
   HJ_TRY(mg_level(P, 1, &ec));
   const int flip = (P->mg_nu1 + P->mg_nu2) & 1;
-  HJ_TRY(mg_check(launch_mg_correct(g, P->X[cur], P->X[cur ^ flip], N->g, N->X[ec], P->ctrl, st), "correct"));
-  cur ^= flip;
-  for (int c = 0; c < P->mg_nu2; ++c, cur ^= 1) HJ_TRY(mg_smooth(P, cur, INF, P->ctrl));
+  int c2 = 0;
+  if (g.dim == 2 && P->mg_nu2 > 0 && !flip) {  // correction fused into the first post-smoothing cycle
+    HJ_TRY(mg_smooth(P, cur, INF, P->ctrl, N, ec));
+    cur ^= 1;
+    c2 = 1;
+  } else {
+    HJ_TRY(mg_check(launch_mg_correct(g, P->X[cur], P->X[cur ^ flip], N->g, N->X[ec], P->ctrl, st), "correct"));
+    cur ^= flip;
+  }
+  for (; c2 < P->mg_nu2; ++c2, cur ^= 1) HJ_TRY(mg_smooth(P, cur, INF, P->ctrl));
   if (cur != 0) { set_error("internal: V-cycle parity"); return HJ_ERR_CUDA; }
   if (timed) HJ_CUDA(cudaEventRecord(e1, st));
   return HJ_OK;

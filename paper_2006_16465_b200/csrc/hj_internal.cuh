@@ -110,6 +110,12 @@ struct CycleArgs {
   double* part;               // per-tile residual partials of the snapshot
   const Ctrl* ctrl;
   long long max_cycles;
+  // multigrid (reading c24): if cor_e != NULL, the snapshot is first corrected by the (bi)linear
+  // interpolation of the next coarser iterate cor_e (a padded buffer of pitch cor_pitch) — the
+  // coarse-grid correction fused into the first post-smoothing cycle (2D only)
+  const void* cor_e = nullptr;
+  long long cor_pitch = 0;
+  const CUtensorMap* tm_cor = nullptr;  // REG2D: TMA map of cor_e, box R2::EW x 18 (tile's patch)
 };
 
 // Launchers (kernels_2d.cu / kernels_1d.cu).  Return cudaGetLastError().
@@ -250,6 +256,34 @@ __device__ __forceinline__ float gupd1(float wl, float wr, float L, float R, flo
 }
 __device__ __forceinline__ double gres1(double wl, double wr, double x, double L, double R, double q) {
   return __dsub_rn(gupd1(wl, wr, L, R, q), x);
+}
+
+// Correctly rounded T arithmetic that the compiler may not contract (reading c24 fixes the order).
+template <typename T>
+__device__ __forceinline__ T add_t(T a, T b) {
+  if constexpr (sizeof(T) == 8) return __dadd_rn(a, b);
+  else return __fadd_rn(a, b);
+}
+template <typename T>
+__device__ __forceinline__ T mul_t(T a, T b) {
+  if constexpr (sizeof(T) == 8) return __dmul_rn(a, b);
+  else return __fmul_rn(a, b);
+}
+// (Bi)linear interpolation of the coarse iterate at the fine ringed interior point (i, j) (coarse
+// ringed point I sits on fine 2I; the coarse ring is zero): DESIGN.md reading c24.
+template <typename T, typename F>
+__device__ __forceinline__ T mg_interp_f(F&& E, long long i, long long j) {
+  const bool ci = (i & 1) == 0, cj = (j & 1) == 0;
+  if (ci && cj) return E(i / 2, j / 2);
+  if (cj) return mul_t(T(0.5), add_t(E((i - 1) / 2, j / 2), E((i + 1) / 2, j / 2)));
+  if (ci) return mul_t(T(0.5), add_t(E(i / 2, (j - 1) / 2), E(i / 2, (j + 1) / 2)));
+  return mul_t(T(0.25), add_t(add_t(E((i - 1) / 2, (j - 1) / 2), E((i + 1) / 2, (j - 1) / 2)),
+                              add_t(E((i - 1) / 2, (j + 1) / 2), E((i + 1) / 2, (j + 1) / 2))));
+}
+template <typename T>
+__device__ __forceinline__ T mg_interp(const T* __restrict__ e, long long ep, long long i, long long j) {
+  constexpr int COL0 = 16 / sizeof(T);
+  return mg_interp_f<T>([&](long long I, long long J) { return e[J * ep + (COL0 - 1) + I]; }, i, j);
 }
 
 // Damped Jacobi (multigrid smoother, reading c24): x + omega (u - x) as ONE fma in T.

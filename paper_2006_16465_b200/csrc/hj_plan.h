@@ -62,6 +62,7 @@ struct hj_plan {
   CUtensorMap tmX[2];   // loads: 34-row box with halo
   CUtensorMap tmXs[2];  // stores: 32x32 interior box
   CUtensorMap tmF;
+  CUtensorMap tmE[2];   // multigrid coarse level (2D): patch boxes for the fused correction
   std::map<int, cudaGraphExec_t> graphs;
   long long c_host = 0;
   std::vector<cudaEvent_t> evpool;  // timed runs: (start, end) per cycle kernel

@@ -46,7 +46,15 @@ struct R2 {
   static constexpr bool TMA_STORE = TMA_STORE_;
   static constexpr int OBYTES = TMA_STORE ? 32 * 32 * sizeof(T) : 0;   // output staging tile
   static constexpr int HALO = 128 * sizeof(T);                          // frozen halo W|E|S|N
-  static constexpr int WSMEM = XSLOT + FBYTES + OBYTES + HALO;          // per warp
+  // multigrid fused correction: the 18 x 18 coarse patch under the tile + halo (TMA box).  TMA box
+  // origins must be 16-B aligned along x, so the box starts COL0 - 1 elements before the patch's
+  // first ringed column (at element x0/2 of the padded row) and is COL0 - 1 + 18 wide, rounded
+  // up to a 16-B multiple.
+  static constexpr int EW = sizeof(T) == 8 ? 20 : 24, EH = 18;
+  static constexpr int EBYTES = EW * EH * sizeof(T);
+  static constexpr int ESLOT = (EBYTES + 127) / 128 * 128;
+  static constexpr int EOFF = XSLOT + FBYTES + OBYTES + HALO;
+  static constexpr int WSMEM = EOFF + ESLOT;                            // per warp
   static constexpr int WARPS = WARPS_;
   static constexpr int BARS = 128;                                      // barrier region bytes
   static constexpr size_t SMEM = 128 + BARS + size_t(WARPS) * WSMEM;    // +128 for alignment
@@ -177,12 +185,13 @@ struct Tile2 {
 };
 
 // One full 32x32 tile: smem slot -> registers, refill, fused residual, k sub-iterations, store.
-template <typename T, typename C, bool MASK, int SK, typename Refill, typename Store>
+template <typename T, typename C, bool MASK, int SK, bool COR, typename Refill, typename Store>
 __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ sx, const T* __restrict__ sf,
                                            T* __restrict__ so, T* __restrict__ hb, int lane, int kk,
                                            double* __restrict__ part, long long t, Refill&& refill,
                                            Store&& store, T* __restrict__ gdst, long long pitch,
-                                           int ox0, int ox1, int oy0, int oy1) {
+                                           int ox0, int ox1, int oy0, int oy1, const T* __restrict__ eb,
+                                           int x0, int y0, int nx, int ny) {
   using V2 = typename VecOf<T>::v2;
   const int lx = lane & 7, ly = lane >> 3;
   Tile2<T, MASK, SK> tl;
@@ -200,10 +209,48 @@ __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ 
     tl.q[i][0] = fa.x; tl.q[i][1] = fa.y; tl.q[i][2] = fb.x; tl.q[i][3] = fb.y;
   }
   // frozen halo -> the warp's halo buffer [W(32) | E(32) | S(32) | N(32)]
-  hb[lane] = sx[(lane + 1) * C::BW + C::COL0 - 1];
-  hb[32 + lane] = sx[(lane + 1) * C::BW + C::COL0 + 32];
-  hb[64 + lane] = sx[C::COL0 + lane];
-  hb[96 + lane] = sx[33 * C::BW + C::COL0 + lane];
+  T hw = sx[(lane + 1) * C::BW + C::COL0 - 1];
+  T he = sx[(lane + 1) * C::BW + C::COL0 + 32];
+  T hs = sx[C::COL0 + lane];
+  T hn = sx[33 * C::BW + C::COL0 + lane];
+  if constexpr (COR) {
+    // multigrid: correct the snapshot (tile and halo) by the interpolated coarse iterate before
+    // anything reads it — the coarse-grid correction fused into this post-smoothing cycle (c24).
+    // The coarse patch under tile + halo (ringed coarse rows y0/2 .., columns x0/2 ..) arrived
+    // with the tile by TMA (eb, row stride EW); lane patch = rows 4ly .. +4, columns 2lx .. +2.
+    T E[5][3];
+#pragma unroll
+    for (int r = 0; r < 5; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) E[r][c] = eb[(4 * ly + r) * C::EW + (C::COL0 - 1) + 2 * lx + c];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int a = i / 2, b = c / 2;  // fine row i / col c of the lane: odd ringed index when even
+        T v;
+        if ((i & 1) == 0 && (c & 1) == 0)
+          v = mul_t(T(0.25), add_t(add_t(E[a][b], E[a][b + 1]), add_t(E[a + 1][b], E[a + 1][b + 1])));
+        else if ((i & 1) == 0)
+          v = mul_t(T(0.5), add_t(E[a][(c + 1) / 2], E[a + 1][(c + 1) / 2]));
+        else if ((c & 1) == 0)
+          v = mul_t(T(0.5), add_t(E[(i + 1) / 2][b], E[(i + 1) / 2][b + 1]));
+        else
+          v = E[(i + 1) / 2][(c + 1) / 2];
+        tl.x[i][c] = add_t(tl.x[i][c], v);
+      }
+    // halo points inside the domain (the domain ring holds g and is never corrected); tile-local
+    // ringed coordinates (a, b) in [0, 33] have the parity of the global ones (x0, y0 even)
+    auto EB = [&](int I, int J) { return eb[J * C::EW + (C::COL0 - 1) + I]; };
+    if (x0 > 0) hw = add_t(hw, mg_interp_f<T>(EB, 0, lane + 1));
+    if (x0 + 32 < nx) he = add_t(he, mg_interp_f<T>(EB, 33, lane + 1));
+    if (y0 > 0) hs = add_t(hs, mg_interp_f<T>(EB, lane + 1, 0));
+    if (y0 + 32 < ny) hn = add_t(hn, mg_interp_f<T>(EB, lane + 1, 33));
+  }
+  hb[lane] = hw;
+  hb[32 + lane] = he;
+  hb[64 + lane] = hs;
+  hb[96 + lane] = hn;
   tl.hxp = hb + (lx == 0 ? 0 : 32) + 8 * ly;
   tl.hyp = hb + (ly == 0 ? 64 : 96) + 4 * lx;
   tl.own = 0xffffffffu;
@@ -278,12 +325,13 @@ __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ 
 // Persistent kernel over the FULL 32x32 tiles (ntx_full x nty_full of them; ragged edge tiles,
 // if any, are done by smem2d_kernel in edge mode).  Warp w handles full tiles w, w+W, ...;
 // partials are indexed by the global tile index ty*ntx + tx.
-template <typename T, typename C, bool MASK, int SK>
+template <typename T, typename C, bool MASK, int SK, bool COR = false>
 __global__ void __launch_bounds__(C::WARPS * 32, 1)
 reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
              const __grid_constant__ CUtensorMap tmO, T* __restrict__ xout, long long pitch,
              Axis ax, Axis ay, int ntx_full, long long nfull, int ntx, double* __restrict__ part,
-             const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt) {
+             const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt,
+             const __grid_constant__ CUtensorMap tmE) {
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
   extern __shared__ unsigned char smem_raw[];
@@ -296,14 +344,16 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
   const T* sf = reinterpret_cast<const T*>(slot + C::XSLOT);
   T* so = reinterpret_cast<T*>(slot + C::XSLOT + C::FBYTES);
   T* hb = reinterpret_cast<T*>(slot + C::XSLOT + C::FBYTES + C::OBYTES);
+  const T* eb = reinterpret_cast<const T*>(slot + C::EOFF);
   const long long gw = (long long)blockIdx.x * C::WARPS + warp;
   const long long nw = (long long)gridDim.x * C::WARPS;
   if (gw >= nfull) return;
   auto issue = [&](long long u) {  // u: full-block index; box origin = block's interior origin
     const int cx = axis_start(ax, (int)(u % ntx_full)), cy = axis_start(ay, (int)(u / ntx_full));
-    mbar_arrive_expect_tx(bar, C::XBYTES + C::FBYTES);
+    mbar_arrive_expect_tx(bar, C::XBYTES + C::FBYTES + (COR ? C::EBYTES : 0));
     tma_load_2d(slot, &tmX, cx, cy, bar);              // x box: padded rows 32ty.., cols 32tx..
     tma_load_2d(slot + C::XSLOT, &tmF, cx, cy, bar);   // h2f box
+    if (COR) tma_load_2d(slot + C::EOFF, &tmE, cx / 2, cy / 2, bar);  // coarse patch (16-B aligned start)
   };
   if (lane == 0) {
     mbar_init(bar, 1);
@@ -311,6 +361,7 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
     prefetch_tensormap(&tmX);
     prefetch_tensormap(&tmF);
     prefetch_tensormap(&tmO);
+    if (COR) prefetch_tensormap(&tmE);
     issue(gw);
   }
   __syncwarp();
@@ -319,7 +370,7 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
     mbar_wait(bar, it & 1);
     const int tx = (int)(u % ntx_full), ty = (int)(u / ntx_full);
     const int x0 = axis_start(ax, tx), y0 = axis_start(ay, ty);
-    reg2d_tile<T, C, MASK, SK>(
+    reg2d_tile<T, C, MASK, SK, COR>(
         wt, sx, sf, so, hb, lane, kk, part, (long long)ty * ntx + tx,
         [&] {
           if (lane == 0 && u + nw < nfull) {
@@ -334,7 +385,8 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
           }
         },
         xout + ((long long)y0 + 1) * pitch + C::COL0 + x0, pitch, axis_own_lo(ax, tx) - x0,
-        axis_own_hi(ax, tx) - x0, axis_own_lo(ay, ty) - y0, axis_own_hi(ay, ty) - y0);
+        axis_own_hi(ax, tx) - x0, axis_own_lo(ay, ty) - y0, axis_own_hi(ay, ty) - y0, eb, x0, y0,
+        ax.n, ay.n);
   }
   if (C::TMA_STORE && lane == 0) bulk_wait_all();
 }
@@ -351,7 +403,8 @@ template <typename T, int SK>
 __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
                               const T* __restrict__ h2f, long long pitch, long long fpitch, int nx,
                               int ny, Axis ax, Axis ay, int edge, double* __restrict__ part,
-                              const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt) {
+                              const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt,
+                              const T* __restrict__ ecor, long long ep) {
   constexpr bool GEN = SK == 1;  // general coefficients (reading c23)
   const int ntx = ax.nb, nty = ay.nb;
   if (ctrl->done) return;
@@ -385,6 +438,8 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
     const long long gi = i0 + a, gj = j0 + b; // padded coordinates (ring at 0)
     T v = T(0);
     if (gi <= nx + 1 && gj <= ny + 1) v = xin[gj * pitch + (COL0 - 1) + gi];
+    // multigrid: fused coarse-grid correction of the interior points (reading c24)
+    if (ecor && gi >= 1 && gi <= nx && gj >= 1 && gj <= ny) v = add_t(v, mg_interp(ecor, ep, gi, gj));
     A[q] = v;
     B[q] = v;
   }
@@ -538,26 +593,38 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
     const long long ntx_full = ovl ? g.ntx : g.nx / 32, nty_full = ovl ? g.nty : g.ny / 32;
     const long long nfull = ntx_full * nty_full;
     if (nfull > 0) {
-      auto go = [&](auto cfg, auto mask) {
+      auto go = [&](auto cfg, auto mask, auto cor) {
         using C = decltype(cfg);
         long long ctas = (nfull + C::WARPS - 1) / C::WARPS;
         if (ctas > grid_hint) ctas = grid_hint;
-        reg2d_kernel<T, C, decltype(mask)::value, SK><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
-            *a.tm_in, *a.tm_f, *a.tm_out, (T*)a.xout, g.pitch, g.ax, g.ay, (int)ntx_full, nfull,
-            (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles, wt);
+        reg2d_kernel<T, C, decltype(mask)::value, SK, decltype(cor)::value>
+            <<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
+                *a.tm_in, *a.tm_f, *a.tm_out, (T*)a.xout, g.pitch, g.ax, g.ay, (int)ntx_full, nfull,
+                (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles, wt, a.tm_cor ? *a.tm_cor : *a.tm_in);
       };
-      if (ovl) go(R2<T>{}, std::true_type{});
-      else go(R2<T>{}, std::false_type{});
+      if constexpr (SK == 2) {
+        if (a.cor_e) {  // multigrid post-smoothing with the fused coarse-grid correction (o = 0)
+          if (ovl || !a.tm_cor) return cudaErrorInvalidValue;
+          go(R2<T>{}, std::false_type{}, std::true_type{});
+        } else if (ovl) {
+          go(R2<T>{}, std::true_type{}, std::false_type{});
+        } else {
+          go(R2<T>{}, std::false_type{}, std::false_type{});
+        }
+      } else {
+        if (ovl) go(R2<T>{}, std::true_type{}, std::false_type{});
+        else go(R2<T>{}, std::false_type{}, std::false_type{});
+      }
     }
     const long long nedge = g.ntiles - nfull;
     if (nedge > 0)
       smem2d_kernel<T, SK><<<(unsigned)nedge, dim3(32, 32), smem_paper, st>>>(
           (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
-          g.ax, g.ay, 1, a.part, a.ctrl, g.k, a.max_cycles, wt);
+          g.ax, g.ay, 1, a.part, a.ctrl, g.k, a.max_cycles, wt, (const T*)a.cor_e, a.cor_pitch);
   } else if (g.kernel_kind == K_SMEM2D) {
     smem2d_kernel<T, SK><<<(unsigned)g.ntiles, dim3(g.tx, g.ty), smem_paper, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
-        g.ax, g.ay, 0, a.part, a.ctrl, g.k, a.max_cycles, wt);
+        g.ax, g.ay, 0, a.part, a.ctrl, g.k, a.max_cycles, wt, (const T*)a.cor_e, a.cor_pitch);
   } else {
     classic2d_kernel<T, SK == 1><<<(unsigned)(g.ntx * g.nty), 128, 0, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
@@ -577,6 +644,11 @@ cudaError_t cfg2() {
   e = cudaFuncSetAttribute(reg2d_kernel<T, C, true, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)C::SMEM);
   if (e != cudaSuccess) return e;
+  if constexpr (SK == 2) {
+    e = cudaFuncSetAttribute(reg2d_kernel<T, C, false, SK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+  }
   return cudaFuncSetAttribute(smem2d_kernel<T, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 

@@ -126,17 +126,6 @@ mg_restrict2d_stream(const T* __restrict__ xf, const T* __restrict__ qf, long lo
   }
 }
 
-template <typename T>
-__device__ __forceinline__ T add_t(T a, T b) {
-  if constexpr (sizeof(T) == 8) return __dadd_rn(a, b);
-  else return __fadd_rn(a, b);
-}
-template <typename T>
-__device__ __forceinline__ T mul_t(T a, T b) {
-  if constexpr (sizeof(T) == 8) return __dmul_rn(a, b);
-  else return __fmul_rn(a, b);
-}
-
 // Vectorised correction: thread (Ir, Jr) (ringed coarse, 0..nxc x 0..nyc) updates the fine 2x2
 // block at ringed (2Ir+1, 2Ir+2) x (2Jr+1, 2Jr+2) from the four coarse values around it, with one
 // 2-wide vector load and store per fine row (interior column 2Ir is 16-B aligned in f64, 8-B in f32).
