@@ -43,6 +43,9 @@ def parse():
                     help="also measure time-to-tolerance at this relative tol (0 = skip)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-mg", action="store_true", help="skip the multigrid time-to-1e-6 leg")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N>1 exchange: the library's peer-memory kernels (CUDA IPC over NVLink; falls "
+                         "back to NCCL if the mapping cannot be set up) or NCCL send/recv + allreduce")
     return ap.parse_args()
 
 
@@ -214,10 +217,27 @@ def main():
     import torch.distributed as dist
     from paper_2006_16465_b200 import hj
 
+    # HJ_BENCH_ONE_GPU=1 (testing only): every rank on cuda:0 with a gloo process group, so the
+    # N>1 code path (peer transport between processes) can be exercised on a one-GPU box; its
+    # timings are meaningless (the ranks share one GPU)
+    one_gpu = os.environ.get("HJ_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def allreduce(t, op):
+        if one_gpu:
+            c = t.cpu()
+            dist.all_reduce(c, op=op)
+            t.copy_(c)
+        else:
+            dist.all_reduce(t, op=op)
     n, k = args.n, (args.k if args.mode == "hier" else 1)
     h = 1.0 / (n + 1)
     # row slab of this rank (whole tile rows; PAPER-faithful tiles never straddle ranks)
@@ -231,11 +251,36 @@ def main():
     sobj = torch.cuda.Stream(dev)          # the plan's stream: graphs and timing events live here
     stream = sobj.cuda_stream
     torch.cuda.synchronize()               # inputs were written on torch's stream
+    transport = None
     if world > 1:
-        idb = [hj.hj_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(idb, src=0)
-        plan = hj.DistPlan(n, n, h, f, bc, x0, rank=rank, nranks=world, nccl_id=idb[0], row_begin=rb,
-                           row_end=re, stream=stream, **prm)
+        plan = None
+        if args.transport == "peer":
+            # peer-memory transport: halo rows, residual row sums and the per-cycle signal are stored
+            # by the library's kernels into the neighbours' buffers (CUDA IPC over NVLink), no NCCL
+            ok = 1
+            try:
+                plan = hj.PeerPlan(n, n, h, f, bc, x0, rank=rank, nranks=world, row_begin=rb, row_end=re,
+                                   stream=stream, **prm)
+                plan.connect()
+                plan.run(2)
+                torch.cuda.synchronize()
+            except Exception as e:  # noqa: BLE001 - report and fall back collectively
+                print(f"rank {rank}: peer transport unavailable ({e}); falling back to NCCL", file=sys.stderr)
+                ok = 0
+            okt = torch.tensor([ok], dtype=torch.int32, device=dev)
+            allreduce(okt, dist.ReduceOp.MIN)
+            if okt.item() == 1:
+                transport = "peer-memory (CUDA IPC, library kernels)"
+            else:
+                if plan is not None:
+                    plan.close()
+                plan = None
+        if plan is None:
+            idb = [hj.hj_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(idb, src=0)
+            plan = hj.DistPlan(n, n, h, f, bc, x0, rank=rank, nranks=world, nccl_id=idb[0], row_begin=rb,
+                               row_end=re, stream=stream, **prm)
+            transport = "nccl (send/recv halos + allreduce)"
     else:
         plan = hj.Plan(2, n, n, h, f, bc, x0, stream=stream, **prm)
     torch.cuda.synchronize()
@@ -259,7 +304,7 @@ def main():
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms, kernel_ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allreduce(t, dist.ReduceOp.MAX)
     ms, kernel_ms = t.tolist()
     ms_step = ms / args.steps
     kern_ms = kernel_ms / args.steps
@@ -295,7 +340,7 @@ def main():
         ttt = {"tol": args.ttt, "protocol": "P (f=1, x0=1, g=0)", "cycles": r["cycles"],
                "converged": r["converged"], "seconds": r["seconds_solve"], "seconds_with_transfers": sec,
                "measured": True}
-    elif world > 1 and args.ttt > 0:
+    elif world > 1 and args.ttt > 0 and not one_gpu:
         # each rank solves its slab from pinned host buffers (jacobi_solve_dist); max over ranks
         fh = torch.ones(nloc * n, dtype=torch.float64).pin_memory()
         xh = torch.ones(nloc * n, dtype=torch.float64).pin_memory()
@@ -308,7 +353,7 @@ def main():
                                  nccl_id=idb[0], row_begin=rb, row_end=re, history=False, mode=args.mode,
                                  tile=(TILE, TILE), k=k, tol=args.ttt, max_cycles=10**7, kernel=args.kernel)
         tt = torch.tensor([time.perf_counter() - t0, r["seconds_solve"]], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        allreduce(tt, dist.ReduceOp.MAX)
         sec, ssolve = tt.tolist()
         cyc = max(r["cycles"], 1)
         e2e = {"value": n * n * k * cyc / sec, "unit": "cell-updates/s",
@@ -356,6 +401,7 @@ def main():
            "config": {"workload": f"cfg4: 2D Poisson {n}^2 fp64, {TILE}x{TILE} tiles, k={k}, mode={args.mode}, "
                                   f"paper protocol f=1 x0=1", "grid": n, "tile": [TILE, TILE], "k": k,
                       "mode": args.mode, "kernel": args.kernel, "parallelism": f"row-slab x{world}",
+                      "transport": transport,
                       "l2": "inputs 6.4 GB >> 126 MB L2, no flush needed"},
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak, "traffic": ncu_traffic(), "peak_source": peak_src,

@@ -55,8 +55,9 @@ def main():
     sizes = [1023, 4095, 16383] if not a.quick else [1023]
     for n in sizes:
         for proto in ("P", "M"):
-            for k, nu1, nu2 in ((4, 1, 1), (2, 1, 1), (8, 1, 1), (4, 2, 2), (1, 1, 1)):
-                if n == 16383 and (k, nu1, nu2) not in ((4, 1, 1), (2, 1, 1), (1, 1, 1)):
+            for k, nu1, nu2 in ((4, 1, 1), (2, 1, 1), (8, 1, 1), (4, 2, 2), (4, 2, 1), (4, 1, 2),
+                                (2, 2, 2), (4, 3, 3), (1, 1, 1)):
+                if n == 1023 and (nu1, nu2) != (1, 1):
                     continue
                 r = run(n, proto, 1e-6, k, nu1, nu2)
                 rows.append(r)
