@@ -35,7 +35,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=6)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_GRID)
+    ap.add_argument("--grid", dest="n", type=int, default=N_GRID)
     ap.add_argument("--k", type=int, default=K_SUB)
     ap.add_argument("--mode", default="hier", choices=["hier", "classic"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "smem"])
@@ -402,7 +402,9 @@ def main():
                                   f"paper protocol f=1 x0=1", "grid": n, "tile": [TILE, TILE], "k": k,
                       "mode": args.mode, "kernel": args.kernel, "parallelism": f"row-slab x{world}",
                       "transport": transport,
-                      "l2": "inputs 6.4 GB >> 126 MB L2, no flush needed"},
+                      "l2": f"inputs {3 * 8 * n * n / world / 1e9:.2f} GB per GPU vs 126 MB L2"
+                            + (", no flush needed" if 3 * 8 * n * n / world > 4 * 126e6 else
+                               " (L2-resident: not an HBM measurement)")},
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak, "traffic": ncu_traffic(), "peak_source": peak_src,
                         "kernel_ms": kern_ms, "bytes_per_cell": BYTES_PER_CELL,
