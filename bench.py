@@ -27,6 +27,9 @@ N_GRID = 16384
 TILE = 32
 K_SUB = 16
 BYTES_PER_CELL = 24  # x_c read 8 + h2f read 8 + x_{c+1} write 8
+# FP64 instruction rate of one B200 (148 SMs x 64 FP64 lanes x 1.965 GHz boost; a DFMA or DADD
+# counts one op): the cycle does 4k + 3 FP64 ops per cell
+FP64_PEAK_OPS = 148 * 64 * 1.965e9
 
 
 def parse():
@@ -320,6 +323,35 @@ def main():
         classic_ms = cplan.run(20, timed=True) / 20
         cplan.close()
 
+    # the north star's "load/store phase" target (>= 70% of the HBM roofline): the same cycle
+    # kernel with k = 1 and k = 4 sub-iterations (24 B/cell either way; at k = 16 the kernel is
+    # co-limited by the FP64 pipe), CUDA events around each launch
+    ls_phase = None
+    if args.mode == "hier":
+        ls_phase = {}
+        for kp in (1, 4):
+            pp = dict(prm, k=kp)
+            if world > 1 and transport and transport.startswith("peer"):
+                lp = hj.PeerPlan(n, n, h, f, bc, x0, rank=rank, nranks=world, row_begin=rb, row_end=re,
+                                 stream=stream, **pp)
+                lp.connect()
+            elif world > 1:
+                idl = [hj.hj_nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(idl, src=0)
+                lp = hj.DistPlan(n, n, h, f, bc, x0, rank=rank, nranks=world, nccl_id=idl[0], row_begin=rb,
+                                 row_end=re, stream=stream, **pp)
+            else:
+                lp = hj.Plan(2, n, n, h, f, bc, x0, stream=stream, **pp)
+            lp.run(3, timed=True)
+            kms = lp.run(20, timed=True) / 20
+            lp.close()
+            tk = torch.tensor([kms], dtype=torch.float64, device=dev)
+            if world > 1:
+                allreduce(tk, dist.ReduceOp.MAX)
+            kms = tk.item()
+            ach = BYTES_PER_CELL * n * n / world / (kms * 1e-3) / 1e9
+            ls_phase[f"k{kp}"] = {"kernel_ms": kms, "achieved_gbs": ach}
+
     # end to end through the public C-ABI, the way the paper times it: one
     # jacobi_solve from pinned host buffers to the paper's tolerance, H2D of f/x0 and D2H of x
     # inside the timed region.  Its device-loop time is the measured time-to-tolerance.
@@ -375,6 +407,9 @@ def main():
         return
     peak, peak_src = measured_peaks()
     achieved = BYTES_PER_CELL * n * n / world / (kern_ms * 1e-3) / 1e9   # per-GPU kernel GB/s
+    if ls_phase:
+        for v in ls_phase.values():
+            v["frac"] = v["achieved_gbs"] / peak
     cpu = None
     if world == 1 and not args.no_cpu:
         side = 8192
@@ -408,7 +443,9 @@ def main():
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak, "traffic": ncu_traffic(), "peak_source": peak_src,
                         "kernel_ms": kern_ms, "bytes_per_cell": BYTES_PER_CELL,
-                        "classic_sweep_ms": classic_ms},
+                        "classic_sweep_ms": classic_ms,
+                        "load_store_phase": ls_phase,
+                        "fp64_pipe_frac": (4 * k + 3) * n * n / world / (kern_ms * 1e-3) / FP64_PEAK_OPS},
            "cpu_baseline": cpu,
            "e2e": e2e,
            "gpu_launches": args.steps * plan.launches_per_cycle_static,

@@ -21,6 +21,10 @@ cases = [
     (1, 1024, 9, dict(mode="hier", tile=32, k=16)),                     # batched 1D, reg1d
     (1, 1000, 5, dict(mode="hier", tile=96, k=3)),                      # batched 1D, smem1d
     (1, 3000, 4, dict(mode="classic")),                                 # batched 1D, classic
+    (2, 127, 95, dict(mode="mg", tile=(32, 32), k=3, nu1=1, nu2=1)),    # multigrid, fused correction
+    (2, 127, 95, dict(mode="mg", tile=(32, 32), k=3, nu1=2, nu2=1, dtype="f32")),  # unfused correction
+    (2, 63, 63, dict(mode="mg", tile=(8, 8), k=2, nu1=0, nu2=2)),        # smem levels, residual-only pass
+    (1, 1023, 3, dict(mode="mg", tile=64, k=3)),                         # 1D multigrid
 ]
 for dim, nx, ny, kw in cases:
     p = make_problem("R", dim, nx, ny) if (dim == 2 or ny == 1) else make_problem("R", 1, nx, batch=ny)
