@@ -734,7 +734,7 @@ int launches_per_cycle(const hj_plan* P) {
     const long long nfull = (g.nx / 32) * (g.ny / 32);
     n = (nfull > 0 ? 1 : 0) + (g.ntiles > nfull ? 1 : 0) + 2;
   }
-  if (P->peer && peer_halo_launches(P)) n += 1;  // peer_halo_kernel
+  if (P->peer && g.kernel_kind != K_REG2D && peer_halo_launches(P)) n += 1;  // peer_halo_kernel
   return n;
 }
 
@@ -873,6 +873,7 @@ hj_status launch_cycle(hj_plan* P, int p, bool timed, float* acc_ms) {
   a.part = P->part;
   a.ctrl = P->ctrl;
   a.max_cycles = P->prm.max_cycles;
+  if (P->peer && g.kernel_kind == K_REG2D) peer_halo_ptrs(P, p ^ 1, &a.peer_lo, &a.peer_hi);
   (void)acc_ms;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
@@ -896,7 +897,7 @@ hj_status launch_cycle(hj_plan* P, int p, bool timed, float* acc_ms) {
   PeerDsts pd{};
   PeerSync ps{};
   if (P->peer) {
-    HJ_TRY(peer_halo(P, p ^ 1));
+    if (g.kernel_kind != K_REG2D) HJ_TRY(peer_halo(P, p ^ 1));  // REG2D: fused into the cycle kernel
     peer_cycle_args(P, &pd, &ps);
   }
   const int wpb = 8;

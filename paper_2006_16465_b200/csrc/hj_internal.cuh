@@ -116,6 +116,11 @@ struct CycleArgs {
   const void* cor_e = nullptr;
   long long cor_pitch = 0;
   const CUtensorMap* tm_cor = nullptr;  // REG2D: TMA map of cor_e, box R2::EW x 18 (tile's patch)
+  // peer transport, fused halo (REG2D plans): interior column 0 of the NEIGHBOURS' ghost rows in
+  // their copy of xout (rank-1's row R+1, rank+1's row 0; NULL at the slab ends).  The kernels
+  // store the new first / last interior row straight into them (NVLink stores), tile by tile.
+  void* peer_lo = nullptr;
+  void* peer_hi = nullptr;
 };
 
 // Launchers (kernels_2d.cu / kernels_1d.cu).  Return cudaGetLastError().

@@ -102,6 +102,7 @@ bool peer_attached(const hj_plan* P);
 int peer_halo_launches(const hj_plan* P);       // 1 if this rank has a neighbour, else 0
 hj_status peer_reset(hj_plan* P);                 // collective: device barriers + initial halos
 hj_status peer_halo(hj_plan* P, int buf);          // push rows 1 and R of X[buf] to the neighbours
+void peer_halo_ptrs(const hj_plan* P, int buf, void** lo, void** hi);  // the neighbours' ghost rows
 void peer_cycle_args(const hj_plan* P, PeerDsts* d, PeerSync* s);
 void peer_free(hj_plan* P);
 }  // namespace hj

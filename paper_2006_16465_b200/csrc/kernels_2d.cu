@@ -191,7 +191,7 @@ __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ 
                                            double* __restrict__ part, long long t, Refill&& refill,
                                            Store&& store, T* __restrict__ gdst, long long pitch,
                                            int ox0, int ox1, int oy0, int oy1, const T* __restrict__ eb,
-                                           int x0, int y0, int nx, int ny) {
+                                           int x0, int y0, int nx, int ny, T* plo, T* phi) {
   using V2 = typename VecOf<T>::v2;
   const int lx = lane & 7, ly = lane >> 3;
   Tile2<T, MASK, SK> tl;
@@ -320,6 +320,22 @@ __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ 
       dst[1] = V2{tl.x[i][2], tl.x[i][3]};
     }
   }
+  // peer transport (row slabs): a tile in the slab's first / last tile row also stores its first /
+  // last row straight into the neighbour's ghost row (NVLink stores through the CUDA-IPC mapping),
+  // so the halo exchange overlaps the cycle tile by tile; the fence orders them before the
+  // finalize kernel's signal
+  if (plo && ly == 0) {
+    V2* d = reinterpret_cast<V2*>(plo + x0 + 4 * lx);
+    d[0] = V2{tl.x[0][0], tl.x[0][1]};
+    d[1] = V2{tl.x[0][2], tl.x[0][3]};
+    __threadfence_system();
+  }
+  if (phi && ly == 3) {
+    V2* d = reinterpret_cast<V2*>(phi + x0 + 4 * lx);
+    d[0] = V2{tl.x[7][0], tl.x[7][1]};
+    d[1] = V2{tl.x[7][2], tl.x[7][3]};
+    __threadfence_system();
+  }
 }
 
 // Persistent kernel over the FULL 32x32 tiles (ntx_full x nty_full of them; ragged edge tiles,
@@ -331,7 +347,7 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
              const __grid_constant__ CUtensorMap tmO, T* __restrict__ xout, long long pitch,
              Axis ax, Axis ay, int ntx_full, long long nfull, int ntx, double* __restrict__ part,
              const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt,
-             const __grid_constant__ CUtensorMap tmE) {
+             const __grid_constant__ CUtensorMap tmE, T* peer_lo, T* peer_hi) {
   if (ctrl->done) return;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
   extern __shared__ unsigned char smem_raw[];
@@ -386,7 +402,7 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
         },
         xout + ((long long)y0 + 1) * pitch + C::COL0 + x0, pitch, axis_own_lo(ax, tx) - x0,
         axis_own_hi(ax, tx) - x0, axis_own_lo(ay, ty) - y0, axis_own_hi(ay, ty) - y0, eb, x0, y0,
-        ax.n, ay.n);
+        ax.n, ay.n, ty == 0 ? peer_lo : nullptr, ty == ay.nb - 1 && y0 + 32 == ay.n ? peer_hi : nullptr);
   }
   if (C::TMA_STORE && lane == 0) bulk_wait_all();
 }
@@ -404,7 +420,7 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
                               const T* __restrict__ h2f, long long pitch, long long fpitch, int nx,
                               int ny, Axis ax, Axis ay, int edge, double* __restrict__ part,
                               const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt,
-                              const T* __restrict__ ecor, long long ep) {
+                              const T* __restrict__ ecor, long long ep, T* peer_lo, T* peer_hi) {
   constexpr bool GEN = SK == 1;  // general coefficients (reading c23)
   const int ntx = ax.nb, nty = ay.nb;
   if (ctrl->done) return;
@@ -483,7 +499,12 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
     T* tmp = cur; cur = nxt; nxt = tmp;
   }
   // Step 3: interior back to global (the next iterate)
-  if (kk > 0 && owned) xout[(j0 + b + 1) * pitch + COL0 + i0 + a] = cur[c];
+  if (kk > 0 && owned) {
+    xout[(j0 + b + 1) * pitch + COL0 + i0 + a] = cur[c];
+    // peer transport: the slab's first / last interior row also into the neighbour's ghost row
+    if (peer_lo && j0 + b == 0) { peer_lo[i0 + a] = cur[c]; __threadfence_system(); }
+    if (peer_hi && j0 + b == ny - 1) { peer_hi[i0 + a] = cur[c]; __threadfence_system(); }
+  }
 }
 
 // =============================================================================
@@ -600,7 +621,8 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
         reg2d_kernel<T, C, decltype(mask)::value, SK, decltype(cor)::value>
             <<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
                 *a.tm_in, *a.tm_f, *a.tm_out, (T*)a.xout, g.pitch, g.ax, g.ay, (int)ntx_full, nfull,
-                (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles, wt, a.tm_cor ? *a.tm_cor : *a.tm_in);
+                (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles, wt, a.tm_cor ? *a.tm_cor : *a.tm_in,
+                (T*)a.peer_lo, (T*)a.peer_hi);
       };
       if constexpr (SK == 2) {
         if (a.cor_e) {  // multigrid post-smoothing with the fused coarse-grid correction (o = 0)
@@ -620,11 +642,13 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
     if (nedge > 0)
       smem2d_kernel<T, SK><<<(unsigned)nedge, dim3(32, 32), smem_paper, st>>>(
           (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
-          g.ax, g.ay, 1, a.part, a.ctrl, g.k, a.max_cycles, wt, (const T*)a.cor_e, a.cor_pitch);
+          g.ax, g.ay, 1, a.part, a.ctrl, g.k, a.max_cycles, wt, (const T*)a.cor_e, a.cor_pitch,
+          (T*)a.peer_lo, (T*)a.peer_hi);
   } else if (g.kernel_kind == K_SMEM2D) {
     smem2d_kernel<T, SK><<<(unsigned)g.ntiles, dim3(g.tx, g.ty), smem_paper, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
-        g.ax, g.ay, 0, a.part, a.ctrl, g.k, a.max_cycles, wt, (const T*)a.cor_e, a.cor_pitch);
+        g.ax, g.ay, 0, a.part, a.ctrl, g.k, a.max_cycles, wt, (const T*)a.cor_e, a.cor_pitch,
+        (T*)a.peer_lo, (T*)a.peer_hi);
   } else {
     classic2d_kernel<T, SK == 1><<<(unsigned)(g.ntx * g.nty), 128, 0, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,

@@ -153,6 +153,11 @@ static hj_status launch_halo(hj_plan* P, int buf, const Ctrl* ctrl) {
 
 hj_status peer_halo(hj_plan* P, int buf) { return launch_halo(P, buf, P->ctrl); }
 
+void peer_halo_ptrs(const hj_plan* P, int buf, void** lo, void** hi) {
+  *lo = P->peer->lo[buf];
+  *hi = P->peer->hi[buf];
+}
+
 hj_status peer_reset(hj_plan* P) {
   PeerState* ps = P->peer;
   if (!ps->attached) return HJ_OK;  // hj_plan_peer_attach runs it
