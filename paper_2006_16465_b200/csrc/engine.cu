@@ -741,8 +741,9 @@ int launches_per_cycle(const hj_plan* P) {
 // One hierarchical cycle of level plan L (X[in] -> X[in^1]) as a multigrid smoother; ctrl is the
 // fine plan's (done check); maxc = LLONG_MAX for the internal cycles, -1 for a residual-only pass.
 static hj_status mg_smooth(hj_plan* L, int in, long long maxc, const Ctrl* ctrl,
-                           const hj_plan* cor = nullptr, int cor_buf = 0) {
+                           const hj_plan* cor = nullptr, int cor_buf = 0, bool zero_x = false) {
   CycleArgs a;
+  a.zero_x = zero_x;
   if (cor) {  // fused coarse-grid correction (2D): the snapshot is x + P e, e = cor->X[cor_buf]
     a.cor_e = cor->X[cor_buf];
     a.cor_pitch = cor->g.pitch;
@@ -772,18 +773,28 @@ static hj_status mg_check(cudaError_t e, const char* what) {
 
 // Coarse level l >= 1 (P->mg[l-1]) of the V-cycle; its iterate starts at zero in X[0] (written by
 // the restriction); *out = the buffer holding its result.
+// 2D coarse levels start from zero without reading it: the first cycle runs in zero-start mode
+// and the restriction does not write the zeros (unless that level's first step is not a cycle).
+static bool mg_zero_start(const hj_plan* P, size_t l) {  // level l >= 1
+  if (P->g.dim != 2) return false;
+  return l == P->mg.size() ? P->mg_coarse > 0 : P->mg_nu1 > 0;
+}
+
 static hj_status mg_level(hj_plan* P, size_t l, int* out) {
   hj_plan* L = P->mg[l - 1];
   const long long INF = LLONG_MAX;
+  const bool z = mg_zero_start(P, l);
   int cur = 0;
   if (l == P->mg.size()) {  // coarsest grid: plain cycles from zero
-    for (int c = 0; c < P->mg_coarse; ++c, cur ^= 1) HJ_TRY(mg_smooth(L, cur, INF, P->ctrl));
+    for (int c = 0; c < P->mg_coarse; ++c, cur ^= 1)
+      HJ_TRY(mg_smooth(L, cur, INF, P->ctrl, nullptr, 0, z && c == 0));
     *out = cur;
     return HJ_OK;
   }
   hj_plan* N = P->mg[l];
-  for (int c = 0; c < P->mg_nu1; ++c, cur ^= 1) HJ_TRY(mg_smooth(L, cur, INF, P->ctrl));
-  HJ_TRY(mg_check(launch_mg_restrict(L->g, L->X[cur], L->H2F, N->g, N->H2F, N->X[0], P->ctrl, P->stream), "restrict"));
+  for (int c = 0; c < P->mg_nu1; ++c, cur ^= 1) HJ_TRY(mg_smooth(L, cur, INF, P->ctrl, nullptr, 0, z && c == 0));
+  HJ_TRY(mg_check(launch_mg_restrict(L->g, L->X[cur], L->H2F, N->g, N->H2F, N->X[0], !mg_zero_start(P, l + 1),
+                                     P->ctrl, P->stream), "restrict"));
   int ec = 0;
   HJ_TRY(mg_level(P, l + 1, &ec));
   int c = 0;
@@ -837,7 +848,8 @@ static hj_status launch_vcycle(hj_plan* P, bool timed) {
   HJ_CUDA(cudaGetLastError());
   for (int c = 1; c < P->mg_nu1; ++c, cur ^= 1) HJ_TRY(mg_smooth(P, cur, INF, P->ctrl));
   hj_plan* N = P->mg[0];
-  HJ_TRY(mg_check(launch_mg_restrict(g, P->X[cur], P->H2F, N->g, N->H2F, N->X[0], P->ctrl, st), "restrict"));
+  HJ_TRY(mg_check(launch_mg_restrict(g, P->X[cur], P->H2F, N->g, N->H2F, N->X[0], !mg_zero_start(P, 1),
+                                     P->ctrl, st), "restrict"));
   int ec = 0;
   HJ_TRY(mg_level(P, 1, &ec));
   const int flip = (P->mg_nu1 + P->mg_nu2) & 1;

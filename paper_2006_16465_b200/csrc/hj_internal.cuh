@@ -121,6 +121,8 @@ struct CycleArgs {
   // store the new first / last interior row straight into them (NVLink stores), tile by tile.
   void* peer_lo = nullptr;
   void* peer_hi = nullptr;
+  // multigrid (c24): the snapshot is identically zero (a coarse level's first cycle) — x is not read
+  bool zero_x = false;
 };
 
 // Launchers (kernels_2d.cu / kernels_1d.cu).  Return cudaGetLastError().
@@ -130,8 +132,10 @@ size_t reg1d_smem_bytes(int dtype, int tile);
 int reg1d_warps_per_cta(int dtype, int tile);
 cudaError_t reg_kernels_configure();  // opt in to large dynamic shared memory
 // Multigrid transfers (mg.cu, reading c24): gf = fine level, gc = the next coarser level.
+// write_zero: also zero the coarse iterate's interior (2D skips it when the coarse level's first
+// cycle runs in zero-start mode, CycleArgs::zero_x; 1D always writes it)
 cudaError_t launch_mg_restrict(const Geom& gf, const void* xf, const void* qf, const Geom& gc, void* qc,
-                               void* xc, const Ctrl* ctrl, cudaStream_t st);
+                               void* xc, bool write_zero, const Ctrl* ctrl, cudaStream_t st);
 cudaError_t launch_mg_correct(const Geom& gf, const void* xin, void* xout, const Geom& gc, const void* e,
                               const Ctrl* ctrl, cudaStream_t st);
 

@@ -185,7 +185,10 @@ struct Tile2 {
 };
 
 // One full 32x32 tile: smem slot -> registers, refill, fused residual, k sub-iterations, store.
-template <typename T, typename C, bool MASK, int SK, bool COR, typename Refill, typename Store>
+// XM (x mode): 0 = the snapshot from the slot; 1 = COR, the snapshot plus the interpolated coarse
+// correction (multigrid post-smoothing, c24); 2 = ZX, the snapshot is identically zero and was not
+// loaded (the first smoothing cycle of a coarse multigrid level: its iterate starts at zero, c24).
+template <typename T, typename C, bool MASK, int SK, int XM, typename Refill, typename Store>
 __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ sx, const T* __restrict__ sf,
                                            T* __restrict__ so, T* __restrict__ hb, int lane, int kk,
                                            double* __restrict__ part, long long t, Refill&& refill,
@@ -193,6 +196,7 @@ __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ 
                                            int ox0, int ox1, int oy0, int oy1, const T* __restrict__ eb,
                                            int x0, int y0, int nx, int ny, T* plo, T* phi) {
   using V2 = typename VecOf<T>::v2;
+  constexpr bool COR = XM == 1, ZX = XM == 2;
   const int lx = lane & 7, ly = lane >> 3;
   Tile2<T, MASK, SK> tl;
   if constexpr (SK == 1) {
@@ -204,15 +208,16 @@ __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ 
     const int r = 8 * ly + i;
     const V2* rowx = reinterpret_cast<const V2*>(sx + (r + 1) * C::BW + C::COL0 + 4 * lx);
     const V2* rowf = reinterpret_cast<const V2*>(sf + r * 32 + 4 * lx);
-    const V2 a = rowx[0], b = rowx[1], fa = rowf[0], fb = rowf[1];
+    const V2 a = ZX ? V2{T(0), T(0)} : rowx[0], b = ZX ? V2{T(0), T(0)} : rowx[1];
+    const V2 fa = rowf[0], fb = rowf[1];
     tl.x[i][0] = a.x; tl.x[i][1] = a.y; tl.x[i][2] = b.x; tl.x[i][3] = b.y;
     tl.q[i][0] = fa.x; tl.q[i][1] = fa.y; tl.q[i][2] = fb.x; tl.q[i][3] = fb.y;
   }
   // frozen halo -> the warp's halo buffer [W(32) | E(32) | S(32) | N(32)]
-  T hw = sx[(lane + 1) * C::BW + C::COL0 - 1];
-  T he = sx[(lane + 1) * C::BW + C::COL0 + 32];
-  T hs = sx[C::COL0 + lane];
-  T hn = sx[33 * C::BW + C::COL0 + lane];
+  T hw = ZX ? T(0) : sx[(lane + 1) * C::BW + C::COL0 - 1];
+  T he = ZX ? T(0) : sx[(lane + 1) * C::BW + C::COL0 + 32];
+  T hs = ZX ? T(0) : sx[C::COL0 + lane];
+  T hn = ZX ? T(0) : sx[33 * C::BW + C::COL0 + lane];
   if constexpr (COR) {
     // multigrid: correct the snapshot (tile and halo) by the interpolated coarse iterate before
     // anything reads it — the coarse-grid correction fused into this post-smoothing cycle (c24).
@@ -341,7 +346,7 @@ __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ 
 // Persistent kernel over the FULL 32x32 tiles (ntx_full x nty_full of them; ragged edge tiles,
 // if any, are done by smem2d_kernel in edge mode).  Warp w handles full tiles w, w+W, ...;
 // partials are indexed by the global tile index ty*ntx + tx.
-template <typename T, typename C, bool MASK, int SK, bool COR = false>
+template <typename T, typename C, bool MASK, int SK, int XM = 0>
 __global__ void __launch_bounds__(C::WARPS * 32, 1)
 reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
              const __grid_constant__ CUtensorMap tmO, T* __restrict__ xout, long long pitch,
@@ -349,6 +354,7 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
              const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt,
              const __grid_constant__ CUtensorMap tmE, T* peer_lo, T* peer_hi) {
   if (ctrl->done) return;
+  constexpr bool COR = XM == 1, ZX = XM == 2;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base =
@@ -366,8 +372,8 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
   if (gw >= nfull) return;
   auto issue = [&](long long u) {  // u: full-block index; box origin = block's interior origin
     const int cx = axis_start(ax, (int)(u % ntx_full)), cy = axis_start(ay, (int)(u / ntx_full));
-    mbar_arrive_expect_tx(bar, C::XBYTES + C::FBYTES + (COR ? C::EBYTES : 0));
-    tma_load_2d(slot, &tmX, cx, cy, bar);              // x box: padded rows 32ty.., cols 32tx..
+    mbar_arrive_expect_tx(bar, (ZX ? 0 : C::XBYTES) + C::FBYTES + (COR ? C::EBYTES : 0));
+    if (!ZX) tma_load_2d(slot, &tmX, cx, cy, bar);    // x box: padded rows 32ty.., cols 32tx..
     tma_load_2d(slot + C::XSLOT, &tmF, cx, cy, bar);   // h2f box
     if (COR) tma_load_2d(slot + C::EOFF, &tmE, cx / 2, cy / 2, bar);  // coarse patch (16-B aligned start)
   };
@@ -386,7 +392,7 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
     mbar_wait(bar, it & 1);
     const int tx = (int)(u % ntx_full), ty = (int)(u / ntx_full);
     const int x0 = axis_start(ax, tx), y0 = axis_start(ay, ty);
-    reg2d_tile<T, C, MASK, SK, COR>(
+    reg2d_tile<T, C, MASK, SK, XM>(
         wt, sx, sf, so, hb, lane, kk, part, (long long)ty * ntx + tx,
         [&] {
           if (lane == 0 && u + nw < nfull) {
@@ -420,7 +426,8 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
                               const T* __restrict__ h2f, long long pitch, long long fpitch, int nx,
                               int ny, Axis ax, Axis ay, int edge, double* __restrict__ part,
                               const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt,
-                              const T* __restrict__ ecor, long long ep, T* peer_lo, T* peer_hi) {
+                              const T* __restrict__ ecor, long long ep, T* peer_lo, T* peer_hi,
+                              int zero_x) {
   constexpr bool GEN = SK == 1;  // general coefficients (reading c23)
   const int ntx = ax.nb, nty = ay.nb;
   if (ctrl->done) return;
@@ -453,7 +460,7 @@ __global__ void smem2d_kernel(const T* __restrict__ xin, T* __restrict__ xout,
     const int a = q % L, b = q / L;          // a: 0..Tx+1, b: 0..Ty+1 (halo included)
     const long long gi = i0 + a, gj = j0 + b; // padded coordinates (ring at 0)
     T v = T(0);
-    if (gi <= nx + 1 && gj <= ny + 1) v = xin[gj * pitch + (COL0 - 1) + gi];
+    if (!zero_x && gi <= nx + 1 && gj <= ny + 1) v = xin[gj * pitch + (COL0 - 1) + gi];
     // multigrid: fused coarse-grid correction of the interior points (reading c24)
     if (ecor && gi >= 1 && gi <= nx && gj >= 1 && gj <= ny) v = add_t(v, mg_interp(ecor, ep, gi, gj));
     A[q] = v;
@@ -624,18 +631,24 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
                 (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles, wt, a.tm_cor ? *a.tm_cor : *a.tm_in,
                 (T*)a.peer_lo, (T*)a.peer_hi);
       };
-      if constexpr (SK == 2) {
-        if (a.cor_e) {  // multigrid post-smoothing with the fused coarse-grid correction (o = 0)
-          if (ovl || !a.tm_cor) return cudaErrorInvalidValue;
-          go(R2<T>{}, std::false_type{}, std::true_type{});
-        } else if (ovl) {
-          go(R2<T>{}, std::true_type{}, std::false_type{});
+      using X0 = std::integral_constant<int, 0>;
+      using X1 = std::integral_constant<int, 1>;
+      using X2 = std::integral_constant<int, 2>;
+      if (a.cor_e || a.zero_x) {  // multigrid: fused correction / zero start (o = 0)
+        if (ovl || (a.cor_e && !a.tm_cor)) return cudaErrorInvalidValue;
+        if constexpr (SK == 2) {
+          if (a.cor_e) go(R2<T>{}, std::false_type{}, X1{});
+          else go(R2<T>{}, std::false_type{}, X2{});
+        } else if constexpr (SK == 0) {
+          if (a.cor_e) return cudaErrorInvalidValue;
+          go(R2<T>{}, std::false_type{}, X2{});
         } else {
-          go(R2<T>{}, std::false_type{}, std::false_type{});
+          return cudaErrorInvalidValue;
         }
+      } else if (ovl) {
+        go(R2<T>{}, std::true_type{}, X0{});
       } else {
-        if (ovl) go(R2<T>{}, std::true_type{}, std::false_type{});
-        else go(R2<T>{}, std::false_type{}, std::false_type{});
+        go(R2<T>{}, std::false_type{}, X0{});
       }
     }
     const long long nedge = g.ntiles - nfull;
@@ -643,12 +656,12 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
       smem2d_kernel<T, SK><<<(unsigned)nedge, dim3(32, 32), smem_paper, st>>>(
           (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
           g.ax, g.ay, 1, a.part, a.ctrl, g.k, a.max_cycles, wt, (const T*)a.cor_e, a.cor_pitch,
-          (T*)a.peer_lo, (T*)a.peer_hi);
+          (T*)a.peer_lo, (T*)a.peer_hi, (int)a.zero_x);
   } else if (g.kernel_kind == K_SMEM2D) {
     smem2d_kernel<T, SK><<<(unsigned)g.ntiles, dim3(g.tx, g.ty), smem_paper, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
         g.ax, g.ay, 0, a.part, a.ctrl, g.k, a.max_cycles, wt, (const T*)a.cor_e, a.cor_pitch,
-        (T*)a.peer_lo, (T*)a.peer_hi);
+        (T*)a.peer_lo, (T*)a.peer_hi, (int)a.zero_x);
   } else {
     classic2d_kernel<T, SK == 1><<<(unsigned)(g.ntx * g.nty), 128, 0, st>>>(
         (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
@@ -669,7 +682,12 @@ cudaError_t cfg2() {
                            (int)C::SMEM);
   if (e != cudaSuccess) return e;
   if constexpr (SK == 2) {
-    e = cudaFuncSetAttribute(reg2d_kernel<T, C, false, SK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(reg2d_kernel<T, C, false, SK, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+  }
+  if constexpr (SK == 0 || SK == 2) {
+    e = cudaFuncSetAttribute(reg2d_kernel<T, C, false, SK, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)C::SMEM);
     if (e != cudaSuccess) return e;
   }

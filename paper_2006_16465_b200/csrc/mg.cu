@@ -43,7 +43,7 @@ template <typename T>
 __global__ void __launch_bounds__(128)
 mg_restrict2d_stream(const T* __restrict__ xf, const T* __restrict__ qf, long long pf, long long fpf,
                      int nx, int ny, T* __restrict__ qc, T* __restrict__ xc, long long pc, long long fpc,
-                     int nxc, int nyc, int RB, const Ctrl* __restrict__ ctrl) {
+                     int nxc, int nyc, int RB, int write_zero, const Ctrl* __restrict__ ctrl) {
   if (ctrl->done) return;
   using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
   constexpr unsigned FULL = 0xffffffffu;
@@ -118,7 +118,7 @@ mg_restrict2d_stream(const T* __restrict__ xf, const T* __restrict__ qf, long lo
       const double B = __dmul_rn(2.0, __dadd_rn(__dadd_rn(sm.a, sm.c), __dadd_rn(sp.b, sn.b)));
       const double C = __dadd_rn(__dadd_rn(sp.a, sp.c), __dadd_rn(sn.a, sn.c));
       qc[(long long)J * fpc + I] = (T)__dmul_rn(0.0625, __dadd_rn(__dadd_rn(A, B), C));
-      xc[(long long)(J + 1) * pc + COL0 + I] = T(0);
+      if (write_zero) xc[(long long)(J + 1) * pc + COL0 + I] = T(0);
     }
     p1 = n1;
     p2 = n2;
@@ -204,7 +204,7 @@ __global__ void mg_correct1d_kernel(const T* xin, T* xout, long long pf, int nx,
 
 template <typename T>
 cudaError_t restrict_t(const Geom& gf, const void* xf, const void* qf, const Geom& gc, void* qc,
-                       void* xc, const Ctrl* ctrl, cudaStream_t st) {
+                       void* xc, bool write_zero, const Ctrl* ctrl, cudaStream_t st) {
   if (gf.dim == 2) {
     // strip height: long strips amortise the 3 re-read rows on big grids, short ones keep the
     // latency chain short (and the grid full) on small ones
@@ -212,7 +212,7 @@ cudaError_t restrict_t(const Geom& gf, const void* xf, const void* qf, const Geo
     const dim3 b(128), g((unsigned)((gc.nx + 128) / 128), (unsigned)((gc.ny + rb - 1) / rb));
     mg_restrict2d_stream<T><<<g, b, 0, st>>>((const T*)xf, (const T*)qf, gf.pitch, gf.fpitch, (int)gf.nx,
                                              (int)gf.ny, (T*)qc, (T*)xc, gc.pitch, gc.fpitch, (int)gc.nx,
-                                             (int)gc.ny, rb, ctrl);
+                                             (int)gc.ny, rb, (int)write_zero, ctrl);
   } else {
     const dim3 b(256), g((unsigned)((gc.nx + 255) / 256), (unsigned)gc.ny);
     mg_restrict1d_kernel<T><<<g, b, 0, st>>>((const T*)xf, (const T*)qf, gf.pitch, gf.fpitch, (T*)qc,
@@ -239,9 +239,9 @@ cudaError_t correct_t(const Geom& gf, const void* xin, void* xout, const Geom& g
 }  // namespace
 
 cudaError_t launch_mg_restrict(const Geom& gf, const void* xf, const void* qf, const Geom& gc, void* qc,
-                               void* xc, const Ctrl* ctrl, cudaStream_t st) {
-  return gf.dtype == HJ_F64 ? restrict_t<double>(gf, xf, qf, gc, qc, xc, ctrl, st)
-                            : restrict_t<float>(gf, xf, qf, gc, qc, xc, ctrl, st);
+                               void* xc, bool write_zero, const Ctrl* ctrl, cudaStream_t st) {
+  return gf.dtype == HJ_F64 ? restrict_t<double>(gf, xf, qf, gc, qc, xc, write_zero, ctrl, st)
+                            : restrict_t<float>(gf, xf, qf, gc, qc, xc, write_zero, ctrl, st);
 }
 
 cudaError_t launch_mg_correct(const Geom& gf, const void* xin, void* xout, const Geom& gc, const void* e,
