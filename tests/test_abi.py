@@ -76,3 +76,42 @@ def test_resource_figures_match_paper_formula():
     assert hj.hj_resource_figures(1, 12, 1, tile=4, k=1)[0] == 3
     assert hj.hj_resource_figures(2, 12, 12, tile=(4, 4), k=1)[0] == 9
     assert hj.hj_resource_figures(1, 1024, 1, tile=1024, k=16, dtype="f64")[2] == 24608
+
+
+@pytest.mark.parametrize("kw", [
+    dict(nx=40, ny=41),                       # even n: no vertex-centred coarse grid (reading c24)
+    dict(nx=41, ny=40),
+    dict(overlap=2),
+    dict(omega=1.5),
+    dict(omega=-0.1),
+    dict(levels=1),
+    dict(nu1=-1),
+    dict(stencil=True),
+])
+def test_multigrid_invalid_configs_rejected_before_device_work(kw):
+    import numpy as np
+    nx, ny = kw.pop("nx", 41), kw.pop("ny", 41)
+    stencil = [-1.0, -1.0, -1.0, -1.0, 4.0] if kw.pop("stencil", False) else None
+    prm = dict(mode="mg", tile=(8, 8), k=4, tol=1e-4, max_cycles=10)
+    prm.update(kw)
+    with pytest.raises(hj.HJError) as ei:
+        hj.jacobi_solve(2, nx, ny, 1.0 / (nx + 1), np.ones(nx * ny), stencil=stencil, **prm)
+    assert ei.value.status == hj.HJ_ERR_INVALID_CONFIG
+
+
+def test_params_struct_layout_matches_header(tmp_path):
+    """The ctypes mirror of hj_params / hj_problem / hj_result / hj_dist has the C layout (gcc)."""
+    import subprocess
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "hj.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(hj_params), '
+                   'offsetof(hj_params, overlap_y), offsetof(hj_params, mg_omega), '
+                   'offsetof(hj_params, mg_levels), sizeof(hj_problem), sizeof(hj_result), sizeof(hj_dist));'
+                   'return 0;}\n')
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = [int(v) for v in subprocess.check_output([str(exe)], text=True).split()]
+    P = hj.hj_params
+    want = [ctypes.sizeof(P), P.overlap_y.offset, P.mg_omega.offset, P.mg_levels.offset,
+            ctypes.sizeof(hj.hj_problem), ctypes.sizeof(hj.hj_result), ctypes.sizeof(hj.hj_dist)]
+    assert got == want
