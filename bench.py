@@ -372,28 +372,53 @@ def main():
         ttt = {"tol": args.ttt, "protocol": "P (f=1, x0=1, g=0)", "cycles": r["cycles"],
                "converged": r["converged"], "seconds": r["seconds_solve"], "seconds_with_transfers": sec,
                "measured": True}
-    elif world > 1 and args.ttt > 0 and not one_gpu:
-        # each rank solves its slab from pinned host buffers (jacobi_solve_dist); max over ranks
+    elif world > 1 and args.ttt > 0:
+        # each rank solves its slab from pinned host buffers to the paper's tolerance, max over
+        # ranks: peer transport = H2D of the slab, plan + IPC attach, solve, D2H inside the timed
+        # region (the jacobi_solve_dist sequence with the library's peer kernels); NCCL transport =
+        # jacobi_solve_dist itself
         fh = torch.ones(nloc * n, dtype=torch.float64).pin_memory()
         xh = torch.ones(nloc * n, dtype=torch.float64).pin_memory()
         bh = torch.zeros(4 * n, dtype=torch.float64).pin_memory()
-        idb = [hj.hj_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(idb, src=0)
+        peer = transport is not None and transport.startswith("peer")
+        idb = [None]
+        if not peer:
+            idb = [hj.hj_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(idb, src=0)
         dist.barrier()
-        t0 = time.perf_counter()
-        r = hj.jacobi_solve_dist(n, n, h, fh.numpy(), bh.numpy(), xh.numpy(), rank=rank, nranks=world,
-                                 nccl_id=idb[0], row_begin=rb, row_end=re, history=False, mode=args.mode,
-                                 tile=(TILE, TILE), k=k, tol=args.ttt, max_cycles=10**7, kernel=args.kernel)
-        tt = torch.tensor([time.perf_counter() - t0, r["seconds_solve"]], dtype=torch.float64, device=dev)
+        try:
+            t0 = time.perf_counter()
+            if peer:
+                fd, xd, bd = fh.to(dev, non_blocking=True), xh.to(dev, non_blocking=True), bh.to(dev, non_blocking=True)
+                ep = hj.PeerPlan(n, n, h, fd, bd, xd, rank=rank, nranks=world, row_begin=rb, row_end=re,
+                                 stream=stream, mode=args.mode, tile=(TILE, TILE), k=k, tol=args.ttt,
+                                 max_cycles=10**7, kernel=args.kernel)
+                ep.connect()
+                r = ep.solve(history=False)
+                xout = r["x"].to("cpu")
+                ep.close()
+            else:
+                r = hj.jacobi_solve_dist(n, n, h, fh.numpy(), bh.numpy(), xh.numpy(), rank=rank, nranks=world,
+                                         nccl_id=idb[0], row_begin=rb, row_end=re, history=False, mode=args.mode,
+                                         tile=(TILE, TILE), k=k, tol=args.ttt, max_cycles=10**7, kernel=args.kernel)
+            tt = torch.tensor([time.perf_counter() - t0, r["seconds_solve"], r["cycles"]], dtype=torch.float64,
+                              device=dev)
+        except Exception as e:  # noqa: BLE001 - keep the device-timed line; report the e2e failure
+            print(f"rank {rank}: e2e leg failed: {e}", file=sys.stderr)
+            tt = torch.tensor([-1.0, -1.0, -1.0], dtype=torch.float64, device=dev)
+        tmin = tt.clone()
         allreduce(tt, dist.ReduceOp.MAX)
-        sec, ssolve = tt.tolist()
-        cyc = max(r["cycles"], 1)
-        e2e = {"value": n * n * k * cyc / sec, "unit": "cell-updates/s",
-               "h2d_bytes_per_step": (2 * n * n + 4 * n * world) * 8 / cyc, "d2h_bytes_per_step": n * n * 8 / cyc,
-               "steps": cyc, "seconds": sec, "tol": args.ttt,
-               "api": "jacobi_solve_dist per rank (pinned host buffers) to the paper's tolerance, max over ranks"}
-        ttt = {"tol": args.ttt, "protocol": "P (f=1, x0=1, g=0)", "cycles": r["cycles"],
-               "converged": r["converged"], "seconds": ssolve, "seconds_with_transfers": sec, "measured": True}
+        allreduce(tmin, dist.ReduceOp.MIN)
+        if tmin[0].item() >= 0:
+            sec, ssolve, cyc_f = tt.tolist()
+            cyc = max(int(cyc_f), 1)
+            api = ("peer-transport plan per rank (H2D of the slab, IPC attach, solve, D2H)" if peer else
+                   "jacobi_solve_dist per rank") + " from pinned host buffers to the paper's tolerance, max over ranks"
+            e2e = {"value": n * n * k * cyc / sec, "unit": "cell-updates/s",
+                   "h2d_bytes_per_step": (2 * n * n + 4 * n * world) * 8 / cyc, "d2h_bytes_per_step": n * n * 8 / cyc,
+                   "steps": cyc, "seconds": sec, "tol": args.ttt, "api": api}
+            ttt = {"tol": args.ttt, "protocol": "P (f=1, x0=1, g=0)", "cycles": cyc,
+                   "seconds": ssolve, "seconds_with_transfers": sec, "measured": True}
 
     # the hierarchical cycle as a multigrid smoother — MEASURED time to the
     # north star's 1e-6 on the odd neighbour grid 16383^2 (vertex-centred coarsening needs odd n;
