@@ -199,7 +199,26 @@ def multigrid_leg(dev, stream):
     vc_ms = tp.run(10, timed=True) / 10
     lpc = tp.launches_per_cycle()
     tp.close()
+    # algorithmic HBM bytes of one V-cycle of this schedule: per level with N_l
+    # cells — smoothing 24 B/cell per cycle (16 B for the zero-start first cycle of a coarse
+    # level), restriction 16 B/cell read + 2 B/cell written (coarse q), fused correction +2 B/cell
+    sizes = [n]
+    while sizes[-1] >= 3 and sizes[-1] % 2 == 1:
+        sizes.append((sizes[-1] - 1) // 2)
+    vb = 0.0
+    for l, m in enumerate(sizes):
+        cells = float(m) * m
+        last = l == len(sizes) - 1
+        first = 24.0 if l == 0 else 16.0
+        if last:
+            vb += cells * first
+        else:
+            vb += cells * (first + (18.0 + (24.0 + 2.0)))  # pre (nu1=1), restriction, fused post (nu2=1)
+    peak, _ = measured_peaks()
+    ach = vb / (vc_ms * 1e-3) / 1e9
     return {"tol": 1e-6, "grid": n, "protocol": "P (f=1, x0=1, g=0)", "measured": True,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "algorithmic_bytes_per_vcycle": vb},
             "vcycles": r["cycles"], "converged": r["converged"], "seconds": r["seconds_solve"],
             "ms_per_vcycle": vc_ms, "launches_per_vcycle": lpc,
             "final_rel_residual": hist[-1] / hist[0],
