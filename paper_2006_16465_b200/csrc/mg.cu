@@ -40,7 +40,7 @@ struct XRow {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 8)
 mg_restrict2d_stream(const T* __restrict__ xf, const T* __restrict__ qf, long long pf, long long fpf,
                      int nx, int ny, T* __restrict__ qc, T* __restrict__ xc, long long pc, long long fpc,
                      int nxc, int nyc, int RB, int write_zero, const Ctrl* __restrict__ ctrl) {
