@@ -206,37 +206,7 @@ __global__ void finalize_kernel(const double* __restrict__ R, long long nrg, Ctr
   if (threadIdx.x != 0) return;
   double S = 0.0;
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) S += ws[w];
-  const long long c = ctrl->c;
-  if (hist && c < hist_cap) hist[c] = sqrt(S) / h2;
-  ctrl->S_last = S;
-  if (c == 0) {
-    ctrl->S0 = S;
-    ctrl->sqrtS0 = ref_residual > 0.0 ? ref_residual * h2 : sqrt(S);
-  }
-  bool conv;
-  if (!isfinite(S)) {
-    ctrl->status = HJ_ERR_NUMERIC;
-    ctrl->done = 1;
-    ctrl->c_done = c;
-    return;
-  }
-  const double sq = sqrt(S);
-  const bool test = tol_mode == 0 ? (sq <= tol * ctrl->sqrtS0) : (sq / h2 <= tol);
-  if (c == 0) conv = (S == 0.0) || ((ref_residual > 0.0 || tol_mode == 1) && test);
-  else conv = test;
-  if (conv) {
-    ctrl->done = 1;
-    ctrl->converged = 1;
-    ctrl->status = HJ_OK;
-    ctrl->c_done = c;
-  } else if (c >= max_cycles) {
-    ctrl->done = 1;
-    ctrl->converged = 0;
-    ctrl->status = HJ_NOT_CONVERGED;
-    ctrl->c_done = c;
-  } else {
-    ctrl->c = c + 1;
-  }
+  hj_decide(ctrl, S, hist, hist_cap, h2, tol, tol_mode, ref_residual, max_cycles);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -991,25 +961,72 @@ hj_status plan_run(hj_plan* P, long long ncycles, float* kernel_ms) {
   return HJ_OK;
 }
 
+// The resident solver applies to single-GPU hierarchical 2D plans whose 32x32 tiles fit one per
+// warp of one co-resident wave (8 warps x #SMs): no overlap, nx and ny multiples of 32, Poisson or
+// general coefficients.  HJ_RESIDENT=0 disables it (the per-cycle path, HBM tile loads each cycle).
+static bool resident_ok(const hj_plan* P) {
+  const Geom& g = P->g;
+  if (P->dist || P->peer || !P->mg.empty() || g.omega != 1.0) return false;
+  if (const char* e = std::getenv("HJ_RESIDENT")) if (e[0] == '0') return false;
+  if (g.dim == 1) {  // register 1D plans, tiles of 32..256 points, no ragged tile, <= 1024 problems
+    if (g.kernel_kind != K_REG1D || g.gen || g.ox != 0 || g.tx > 256 || g.nx % g.tx || g.ny > 1024) return false;
+    return (g.nx / g.tx) * g.ny <= 8LL * P->nsm;
+  }
+  // hierarchical register plans only: the classic comparison stays the paper's global-memory sweep
+  if (!(g.kernel_kind == K_REG2D && g.tx == 32 && g.ty == 32 && g.ox == 0 && g.oy == 0)) return false;
+  if (g.nx % 32 || g.ny % 32) return false;
+  return (g.nx / 32) * (g.ny / 32) <= std::min(8LL * P->nsm, 1184LL);
+}
+
+static hj_status run_resident(hj_plan* P, bool* used) {
+  const Geom& g = P->g;
+  *used = false;
+  const long long ntiles = g.dim == 2 ? (g.nx / 32) * (g.ny / 32) : (g.nx / g.tx) * g.ny;
+  if (!P->res_part) {
+    HJ_CUDA(cudaMalloc(&P->res_part, sizeof(double) * 2 * ntiles));
+    HJ_CUDA(cudaMalloc(&P->res_bar, 2 * sizeof(unsigned int)));
+    HJ_CUDA(cudaMemsetAsync(P->res_bar, 0, 2 * sizeof(unsigned int), P->stream));
+  }
+  const int k = g.k;
+  cudaError_t e = (g.dim == 2 ? launch_resident_2d : launch_resident_1d)(
+      g, P->X[0], P->X[1], P->H2F, P->res_part, P->ctrl, P->hist, P->hist_cap, P->prm.tol,
+      (int)P->prm.tol_mode, P->prm.ref_residual, P->prm.max_cycles, k, P->res_bar, P->stream);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {  // not co-resident here: the per-cycle path
+    (void)cudaGetLastError();
+    return HJ_OK;
+  }
+  HJ_CUDA(e);
+  *used = true;
+  return HJ_OK;
+}
+
 hj_status plan_solve(hj_plan* P, hj_result* res, double* x_dev, double* hist_dev) {
   const Geom& g = P->g;
   if (P->peer && !peer_attached(P)) { set_error("peer plan used before hj_plan_peer_attach"); return HJ_ERR_PEER; }
   cudaStream_t st = P->stream;
   HJ_CUDA(cudaEventRecord(P->ev0, st));
-  if (P->c_host & 1) {  // graphs start at even parity
-    HJ_TRY(launch_cycle(P, 1, false, nullptr));
-    P->c_host++;
-  }
-  int G = 2;
-  for (;;) {
-    cudaGraphExec_t ex;
-    HJ_TRY(get_graph(P, G, &ex));
-    HJ_CUDA(cudaGraphLaunch(ex, st));
-    P->c_host += G;
+  bool resident = false;
+  if (resident_ok(P)) HJ_TRY(run_resident(P, &resident));
+  if (resident) {
     HJ_CUDA(cudaMemcpyAsync(P->ctrl_h, P->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     HJ_CUDA(cudaStreamSynchronize(st));
-    if (P->ctrl_h->done) break;
-    if (G < 256) G *= 2;
+    P->c_host = P->ctrl_h->c;
+  } else {
+    if (P->c_host & 1) {  // graphs start at even parity
+      HJ_TRY(launch_cycle(P, 1, false, nullptr));
+      P->c_host++;
+    }
+    int G = 2;
+    for (;;) {
+      cudaGraphExec_t ex;
+      HJ_TRY(get_graph(P, G, &ex));
+      HJ_CUDA(cudaGraphLaunch(ex, st));
+      P->c_host += G;
+      HJ_CUDA(cudaMemcpyAsync(P->ctrl_h, P->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+      HJ_CUDA(cudaStreamSynchronize(st));
+      if (P->ctrl_h->done) break;
+      if (G < 256) G *= 2;
+    }
   }
   HJ_CUDA(cudaEventRecord(P->ev1, st));
   HJ_CUDA(cudaEventSynchronize(P->ev1));
@@ -1044,6 +1061,8 @@ void plan_free(hj_plan* P) {
   for (auto& kv : P->graphs) cudaGraphExecDestroy(kv.second);
   if (P->dist) dist_free(P);
   if (P->peer) peer_free(P);
+  cudaFree(P->res_part);
+  cudaFree(P->res_bar);
   cudaFree(P->X[0]);
   cudaFree(P->X[1]);
   cudaFree(P->H2F);

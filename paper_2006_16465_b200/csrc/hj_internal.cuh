@@ -128,6 +128,15 @@ struct CycleArgs {
 // Launchers (kernels_2d.cu / kernels_1d.cu).  Return cudaGetLastError().
 cudaError_t launch_cycle_2d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st);
 cudaError_t launch_cycle_1d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st);
+// Resident solves (whole solve in one cooperative launch; kernels_2d.cu / kernels_1d.cu): the tiles'
+// iterates stay in registers across cycles, only halos and residual partials cross the grid.
+// part: 2 x ntiles doubles; bar: 2 zeroed unsigned ints.
+cudaError_t launch_resident_2d(const Geom& g, void* X0, void* X1, const void* Q, double* part, Ctrl* ctrl,
+                               double* hist, long long hist_cap, double tol, int tol_mode, double ref_residual,
+                               long long max_cycles, int k, unsigned int* bar, cudaStream_t st);
+cudaError_t launch_resident_1d(const Geom& g, void* X0, void* X1, const void* Q, double* part, Ctrl* ctrl,
+                               double* hist, long long hist_cap, double tol, int tol_mode, double ref_residual,
+                               long long max_cycles, int k, unsigned int* bar, cudaStream_t st);
 size_t reg1d_smem_bytes(int dtype, int tile);
 int reg1d_warps_per_cta(int dtype, int tile);
 cudaError_t reg_kernels_configure();  // opt in to large dynamic shared memory
@@ -301,6 +310,67 @@ __device__ __forceinline__ double damp(double om, double x, double u) {
 }
 __device__ __forceinline__ float damp(float om, float x, float u) {
   return __fmaf_rn(om, __fsub_rn(u, x), x);
+}
+
+// The stopping test of DESIGN.md §3 (c1, c14) for S_c = the summed h^2-scaled squared residual of
+// x_c (h2 = Geom::rdiv): history, S_0, convergence / max_cycles / non-finite; otherwise c + 1.
+// Shared by the engine's finalize_kernel and the resident solvers (one thread).
+__device__ __forceinline__ void hj_decide(Ctrl* ctrl, double S, double* hist, long long hist_cap, double h2,
+                                          double tol, int tol_mode, double ref_residual, long long max_cycles) {
+  const long long c = ctrl->c;
+  if (hist && c < hist_cap) hist[c] = sqrt(S) / h2;
+  ctrl->S_last = S;
+  if (c == 0) {
+    ctrl->S0 = S;
+    ctrl->sqrtS0 = ref_residual > 0.0 ? ref_residual * h2 : sqrt(S);
+  }
+  if (!isfinite(S)) {
+    ctrl->status = HJ_ERR_NUMERIC;
+    ctrl->done = 1;
+    ctrl->c_done = c;
+    return;
+  }
+  const double sq = sqrt(S);
+  const bool test = tol_mode == 0 ? (sq <= tol * ctrl->sqrtS0) : (sq / h2 <= tol);
+  bool conv;
+  if (c == 0) conv = (S == 0.0) || ((ref_residual > 0.0 || tol_mode == 1) && test);
+  else conv = test;
+  if (conv) {
+    ctrl->done = 1;
+    ctrl->converged = 1;
+    ctrl->status = HJ_OK;
+    ctrl->c_done = c;
+  } else if (c >= max_cycles) {
+    ctrl->done = 1;
+    ctrl->converged = 0;
+    ctrl->status = HJ_NOT_CONVERGED;
+    ctrl->c_done = c;
+  } else {
+    ctrl->c = c + 1;
+  }
+}
+
+// Grid-wide barrier of a co-resident (cooperatively launched) grid: bar[0] = arrival count,
+// bar[1] = generation.  Stores before the barrier are visible to loads after it (__threadfence +
+// acquire/release on the generation; readers of other CTAs' data use L2 loads, __ldcg).
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int g;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+    } else {
+      unsigned int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar + 1) : "memory");
+      } while (v == g);
+    }
+  }
+  __syncthreads();
 }
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -73,6 +73,9 @@ struct hj_plan {
   // buffers, Geom and omega; they share this plan's stream and Ctrl for the done check)
   std::vector<hj_plan*> mg;
   int mg_nu1 = 0, mg_nu2 = 0, mg_coarse = 0;
+  // resident solver (launch_resident_2d): residual partials (2 x tiles) and the grid-barrier words
+  double* res_part = nullptr;
+  unsigned int* res_bar = nullptr;
 };
 
 namespace hj {

@@ -195,6 +195,152 @@ reg1d_kernel(const T* __restrict__ xin, T* __restrict__ xout, const T* __restric
 }
 
 // =============================================================================
+// RES1D — the resident 1D solver (see res2d_kernel in kernels_2d.cu): one warp per tile of 32*C
+// points for the whole solve, the tile's points and q in registers across cycles, per cycle only
+// the two frozen halo values of x_c are read (L2) and x_{c+1} written (snapshot semantics); one
+// grid barrier per cycle (a CTA barrier when the grid is one CTA); every CTA reduces the partials
+// in exactly the rowsum_kernel + finalize_kernel order and takes the same stopping decision.
+// Poisson (SK 0) and damped (SK 2) updates, no ragged tiles, rows = independent problems.
+// =============================================================================
+constexpr int RES1D_WARPS = 8;
+template <typename T, int C, int SK>
+__global__ void __launch_bounds__(RES1D_WARPS * 32, 1)
+res1d_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, long long pitch,
+             long long fpitch, int ntpr, int rows, double* __restrict__ part, Ctrl* __restrict__ ctrl,
+             double* __restrict__ hist, long long hist_cap, double rdiv, double tol, int tol_mode,
+             double ref_residual, long long max_cycles, int k, double omd, unsigned int* bar) {
+  constexpr int COL0 = 16 / sizeof(T);
+  constexpr int TILE = 32 * C;
+  __shared__ Ctrl cs;
+  __shared__ int s_done;
+  __shared__ double rsum[1024];   // per-problem residual sums (rows <= 1024)
+  // one-CTA grids: the tiles' boundary values and partials stay in shared memory
+  __shared__ T bnd_l[RES1D_WARPS], bnd_r[RES1D_WARPS];
+  __shared__ double spart[RES1D_WARPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long ntiles = (long long)ntpr * rows;
+  const long long t = (long long)blockIdx.x * RES1D_WARPS + warp;
+  const bool active = t < ntiles;
+  const T om = (T)omd;
+  if (threadIdx.x == 0) {
+    cs = *ctrl;
+    s_done = cs.done;
+  }
+  __syncthreads();
+  if (s_done) return;
+  const long long row = active ? t / ntpr : 0, x0 = active ? (t % ntpr) * (long long)TILE : 0;
+  T x[C], q[C];
+  int p = (int)(cs.c & 1);
+  const bool one = gridDim.x == 1;
+  const long long tr = t % ntpr;  // tile within its row
+  T ring_l = T(0), ring_r = T(0);
+  if (active) {
+    const T* Xc = (p ? X1 : X0) + row * pitch + COL0 + x0 + C * lane;
+    const T* Qr = Q + row * fpitch + x0 + C * lane;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      x[c] = Xc[c];
+      q[c] = Qr[c];
+    }
+    const T* Xr = X0 + row * pitch + COL0;  // the Dirichlet ring (both buffers hold it)
+    ring_l = Xr[-1];
+    ring_r = Xr[(long long)ntpr * TILE];
+    if (one) {
+      if (lane == 0) bnd_l[warp] = x[0];
+      if (lane == 31) bnd_r[warp] = x[C - 1];
+    }
+  }
+  if (one) __syncthreads();
+  for (;;) {
+    const T* Xc = (p ? X1 : X0) + row * pitch + COL0;   // interior point i at Xc[i]; rings at -1, nx
+    T* Xn = (p ? X0 : X1) + row * pitch + COL0;
+    const long long c = cs.c;
+    const int kk = c >= max_cycles ? 0 : k;
+    double* pc = part + (c & 1) * ntiles;
+    if (active) {
+      T hl, hr;  // frozen halo of x_c
+      if (one) {
+        hl = tr == 0 ? ring_l : bnd_r[warp - 1];
+        hr = tr == ntpr - 1 ? ring_r : bnd_l[warp + 1];
+      } else {
+        hl = __ldcg(Xc + x0 - 1);
+        hr = __ldcg(Xc + x0 + TILE);
+      }
+      double acc = 0.0;
+      {
+        T l = __shfl_up_sync(FULL, x[C - 1], 1);
+        T r = __shfl_down_sync(FULL, x[0], 1);
+        if (lane == 0) l = hl;
+        if (lane == 31) r = hr;
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) {
+          const T L = cc == 0 ? l : x[cc - 1];
+          const T R = cc == C - 1 ? r : x[cc + 1];
+          const double s = res1((double)x[cc], (double)L, (double)R, (double)(T(2) * q[cc]));
+          acc = __fma_rn(s, s, acc);
+        }
+      }
+#pragma unroll 1
+      for (int s = 0; s < kk; ++s) {
+        T l = __shfl_up_sync(FULL, x[C - 1], 1);
+        T r = __shfl_down_sync(FULL, x[0], 1);
+        if (lane == 0) l = hl;
+        if (lane == 31) r = hr;
+        T prev = l;
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) {
+          const T R = cc == C - 1 ? r : x[cc + 1];
+          T nv = upd1(prev, R, q[cc]);
+          if constexpr (SK == 2) nv = damp(om, x[cc], nv);
+          prev = x[cc];
+          x[cc] = nv;
+        }
+      }
+      if (kk > 0) {
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) Xn[x0 + C * lane + cc] = x[cc];
+      }
+      acc = warp_sum(acc);
+      if (!one && lane == 0) pc[t] = acc;
+      if (one) {
+        __syncthreads();   // every warp has read this cycle's boundary values
+        if (lane == 0) { spart[warp] = acc; bnd_l[warp] = x[0]; }
+        if (lane == 31) bnd_r[warp] = x[C - 1];
+      }
+    } else if (one) {
+      __syncthreads();
+    }
+    if (one) __syncthreads();
+    else grid_barrier(bar, gridDim.x);
+    // rowsum_kernel + finalize_kernel order (see res2d_kernel): row sums by the CTA's warps, then
+    // finalize's per-warp xor trees over rows 32w .. 32w+31 (rows <= 1024: one row per thread)
+    for (int g = warp; g < rows; g += RES1D_WARPS) {
+      double v = 0.0;
+      for (int qq = lane; qq < ntpr; qq += 32) v += one ? spart[g * ntpr + qq] : __ldcg(pc + (long long)g * ntpr + qq);
+      v = warp_sum(v);
+      if (lane == 0) rsum[g] = v;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double S = 0.0;
+      for (int w = 0; w < 32; ++w) {
+        const int g = 32 * w + lane;
+        S += warp_sum(g < rows ? rsum[g] : 0.0);
+      }
+      if (lane == 0) {
+        hj_decide(&cs, S, blockIdx.x == 0 ? hist : nullptr, hist_cap, rdiv, tol, tol_mode, ref_residual,
+                  max_cycles);
+        s_done = cs.done;
+      }
+    }
+    __syncthreads();
+    if (s_done) break;
+    p ^= 1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ctrl = cs;
+}
+
+// =============================================================================
 // SMEM1D — the paper's Appendix A design: blockDim.x = T threads, shared memory
 // [container 0 (T+2) | container 1 (T+2) | rhs (T)], __syncthreads per
 // sub-iteration, write-back of the latest container (reading c8), into the other global
@@ -399,6 +545,30 @@ cudaError_t configure_1d() {
   HJ_CFG(float)
 #undef HJ_CFG
   return cudaSuccess;
+}
+
+cudaError_t launch_resident_1d(const Geom& g, void* X0, void* X1, const void* Q, double* part, Ctrl* ctrl,
+                               double* hist, long long hist_cap, double tol, int tol_mode, double ref_residual,
+                               long long max_cycles, int k, unsigned int* bar, cudaStream_t st) {
+  int ntpr = (int)(g.nx / g.tx), rows = (int)g.ny;
+  long long pitch = g.pitch, fpitch = g.fpitch;
+  double rdiv = g.rdiv, om = g.omega;
+  void* args[] = {&X0, &X1, &Q, &pitch, &fpitch, &ntpr, &rows, &part, &ctrl, &hist, &hist_cap, &rdiv, &tol,
+                  &tol_mode, &ref_residual, &max_cycles, &k, &om, &bar};
+  const dim3 grid((unsigned)(((long long)ntpr * rows + RES1D_WARPS - 1) / RES1D_WARPS)), block(RES1D_WARPS * 32);
+  const bool f64 = g.dtype == HJ_F64, wgt = g.omega != 1.0;
+  const void* fn = nullptr;
+#define HJ_R1(CC)                                                                                       \
+  case CC:                                                                                              \
+    fn = f64 ? (wgt ? (const void*)res1d_kernel<double, CC, 2> : (const void*)res1d_kernel<double, CC, 0>) \
+             : (wgt ? (const void*)res1d_kernel<float, CC, 2> : (const void*)res1d_kernel<float, CC, 0>);   \
+    break;
+  switch (g.tx / 32) {
+    HJ_R1(1) HJ_R1(2) HJ_R1(4) HJ_R1(8)
+    default: return cudaErrorInvalidValue;
+  }
+#undef HJ_R1
+  return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, st);
 }
 
 cudaError_t launch_cycle_1d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {

@@ -414,6 +414,156 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
 }
 
 // =============================================================================
+// RES2D — the resident solver, for grids whose 32x32 tiles fit one per warp of a co-resident grid
+// (ntiles <= 8 x #SMs, o = 0, nx and ny multiples of 32; BASELINE configs 1 and 3 sizes): the
+// WHOLE solve in one cooperative launch.  Each warp keeps its tile's iterate and q in registers
+// for the entire solve; per cycle it reads only the tile's frozen halo (128 values) of x_c from
+// X[p] (L2), runs the fused residual and the k sub-iterations exactly as reg2d_tile does, writes
+// x_{c+1} into X[p^1] (snapshot semantics: x_c survives a converged test) and its residual
+// partial; one grid barrier; then every CTA sums the partials in the same fixed order and takes
+// the same stopping decision (hj_decide; CTA 0 writes the history and the control block).  Same
+// cycle, same arithmetic — bitwise the iterates of the per-cycle path — without the per-cycle
+// launches and without re-reading the interior.  Classic mode uses it with k = 1 (a hierarchical
+// cycle with k = 1 is the classic sweep, bit for bit: PAPER.md:177, pin P1).
+// =============================================================================
+constexpr int RES2D_MAX_ROWS = 1184;  // tile rows <= tiles <= 8 warps x 148 SMs
+template <typename T, int SK>
+__global__ void __launch_bounds__(256, 1)
+res2d_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, long long pitch,
+             long long fpitch, int ntx, int nty, double* __restrict__ part, Ctrl* __restrict__ ctrl,
+             double* __restrict__ hist, long long hist_cap, double rdiv, double tol, int tol_mode,
+             double ref_residual, long long max_cycles, int k, Wt2 wt, unsigned int* bar) {
+  using V2 = typename VecOf<T>::v2;
+  constexpr int COL0 = 16 / sizeof(T);
+  __shared__ Ctrl cs;
+  __shared__ int s_done;
+  __shared__ __align__(16) T hbuf[8][128];
+  __shared__ double rsum[RES2D_MAX_ROWS];   // tile-row sums of the residual partials
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lx = lane & 7, ly = lane >> 3;
+  const long long ntiles = (long long)ntx * nty;
+  const long long t = (long long)blockIdx.x * 8 + warp;
+  const bool active = t < ntiles;
+  if (threadIdx.x == 0) {
+    cs = *ctrl;
+    s_done = cs.done;
+  }
+  __syncthreads();
+  if (s_done) return;
+  const int tx = active ? (int)(t % ntx) : 0, ty = active ? (int)(t / ntx) : 0;
+  const long long x0 = 32LL * tx, y0 = 32LL * ty;
+  Tile2<T, false, SK> tl;
+  if constexpr (SK == 1) {
+    tl.cw[0] = (T)wt.w; tl.cw[1] = (T)wt.e; tl.cw[2] = (T)wt.s; tl.cw[3] = (T)wt.n;
+  }
+  if constexpr (SK == 2) tl.om = (T)wt.om;
+  tl.own = 0xffffffffu;
+  T* hb = hbuf[warp];
+  tl.hxp = hb + (lx == 0 ? 0 : 32) + 8 * ly;
+  tl.hyp = hb + (ly == 0 ? 64 : 96) + 4 * lx;
+  int p = (int)(cs.c & 1);
+  if (active) {  // the tile's iterate x_c and q, once for the whole solve
+    const T* Xc = p ? X1 : X0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const long long r = 8 * ly + i;
+      const V2* rx = reinterpret_cast<const V2*>(Xc + (y0 + 1 + r) * pitch + COL0 + x0 + 4 * lx);
+      const V2* rf = reinterpret_cast<const V2*>(Q + (y0 + r) * fpitch + x0 + 4 * lx);
+      const V2 a = rx[0], b = rx[1], fa = rf[0], fb = rf[1];
+      tl.x[i][0] = a.x; tl.x[i][1] = a.y; tl.x[i][2] = b.x; tl.x[i][3] = b.y;
+      tl.q[i][0] = fa.x; tl.q[i][1] = fa.y; tl.q[i][2] = fb.x; tl.q[i][3] = fb.y;
+    }
+  }
+  for (;;) {
+    const T* Xc = p ? X1 : X0;
+    T* Xn = p ? X0 : X1;
+    const long long c = cs.c;
+    const int kk = c >= max_cycles ? 0 : k;
+    double* pc = part + (c & 1) * ntiles;   // double-buffered: a slow CTA may still read cycle c-1's
+    if (active) {
+      // frozen halo of x_c: the neighbours' boundary cells written last cycle (L2 loads)
+      hb[lane] = __ldcg(Xc + (y0 + 1 + lane) * pitch + COL0 - 1 + x0);
+      hb[32 + lane] = __ldcg(Xc + (y0 + 1 + lane) * pitch + COL0 + x0 + 32);
+      hb[64 + lane] = __ldcg(Xc + y0 * pitch + COL0 + x0 + lane);
+      hb[96 + lane] = __ldcg(Xc + (y0 + 33) * pitch + COL0 + x0 + lane);
+      __syncwarp();
+      constexpr bool FOLD = sizeof(T) == 8;
+      double acc = 0.0;
+      if (!FOLD || kk == 0) acc = tl.residual(lx, ly);
+      int s = 0;
+      if (FOLD && kk > 0) {
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+        tl.template sweep_mo<true>(lx, ly, a4);
+        acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+        s = 1;
+      }
+      if (s < kk && ((kk - s) & 1)) {
+        tl.template sweep_mo<false>(lx, ly);
+        ++s;
+      }
+#pragma unroll 1
+      for (; s < kk; s += 2) {
+        tl.template sweep_mo<false>(lx, ly);
+        tl.template sweep_mo<false>(lx, ly);
+      }
+      if (kk > 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          V2* dst = reinterpret_cast<V2*>(Xn + (y0 + 1 + 8 * ly + i) * pitch + COL0 + x0 + 4 * lx);
+          dst[0] = V2{tl.x[i][0], tl.x[i][1]};
+          dst[1] = V2{tl.x[i][2], tl.x[i][3]};
+        }
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) pc[t] = acc;
+      __syncwarp();
+    }
+    grid_barrier(bar, gridDim.x);
+    // every CTA: the total in EXACTLY the order of rowsum_kernel + finalize_kernel (so the history
+    // is bitwise that of the per-cycle path): per tile row a lane-strided sum + xor tree, then the
+    // 1024-thread finalize reduction (thread i sums rows i, i+1024, ...; xor tree per warp; the 32
+    // warp sums in order).  Warps split the tile rows; warp 0 finishes.
+    {
+      double* R = rsum;
+      for (int g0 = warp; g0 < nty; g0 += 8 * 4) {  // 4 rows per warp at a time: loads and trees overlap
+        double v[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int g = g0 + 8 * r;
+          v[r] = 0.0;
+          if (g < nty)
+            for (int q = lane; q < ntx; q += 32) v[r] += __ldcg(pc + (long long)g * ntx + q);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) v[r] += __shfl_xor_sync(0xffffffffu, v[r], o);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (lane == 0 && g0 + 8 * r < nty) R[g0 + 8 * r] = v[r];
+      }
+      __syncthreads();
+      if (warp == 0) {
+        double S = 0.0;
+        for (int w = 0; w < 32 && 32 * w < nty; ++w) {  // warps beyond nty add +0.0: S unchanged
+          double v = 0.0;
+          for (int q = 32 * w + lane; q < nty; q += 1024) v += R[q];
+          S += warp_sum(v);
+        }
+        if (lane == 0) {
+          hj_decide(&cs, S, blockIdx.x == 0 ? hist : nullptr, hist_cap, rdiv, tol, tol_mode, ref_residual,
+                    max_cycles);
+          s_done = cs.done;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_done) break;
+    p ^= 1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ctrl = cs;
+}
+
+// =============================================================================
 // SMEM2D — the paper's design (App. A): one CTA per tile, one thread per
 // DOF, two (Tx+2)(Ty+2) containers plus a Tx*Ty rhs array in shared memory (exactly the
 // paper's byte formula), __syncthreads between sub-iterations.  Any tile shape with
@@ -702,6 +852,23 @@ cudaError_t configure_2d() {
   if ((e = cfg2<float, R2<float>, 1>()) != cudaSuccess) return e;
   if ((e = cfg2<double, R2<double>, 2>()) != cudaSuccess) return e;
   return cfg2<float, R2<float>, 2>();
+}
+
+// The resident solve (res2d_kernel), one cooperative launch; k overrides g.k (classic: 1).
+cudaError_t launch_resident_2d(const Geom& g, void* X0, void* X1, const void* Q, double* part, Ctrl* ctrl,
+                               double* hist, long long hist_cap, double tol, int tol_mode, double ref_residual,
+                               long long max_cycles, int k, unsigned int* bar, cudaStream_t st) {
+  int ntx = (int)(g.nx / 32), nty = (int)(g.ny / 32);
+  Wt2 wt{g.wt[0], g.wt[1], g.wt[2], g.wt[3], g.omega};
+  long long pitch = g.pitch, fpitch = g.fpitch;
+  double rdiv = g.rdiv;
+  void* args[] = {&X0, &X1, &Q, &pitch, &fpitch, &ntx, &nty, &part, &ctrl, &hist, &hist_cap, &rdiv, &tol,
+                  &tol_mode, &ref_residual, &max_cycles, &k, &wt, &bar};
+  const dim3 grid((unsigned)((ntx * nty + 7) / 8)), block(256);
+  const void* fn;
+  if (g.dtype == HJ_F64) fn = g.gen ? (const void*)res2d_kernel<double, 1> : (const void*)res2d_kernel<double, 0>;
+  else fn = g.gen ? (const void*)res2d_kernel<float, 1> : (const void*)res2d_kernel<float, 0>;
+  return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, st);
 }
 
 cudaError_t launch_cycle_2d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
