@@ -968,8 +968,8 @@ static bool resident_ok(const hj_plan* P) {
   const Geom& g = P->g;
   if (P->dist || P->peer || !P->mg.empty() || g.omega != 1.0) return false;
   if (const char* e = std::getenv("HJ_RESIDENT")) if (e[0] == '0') return false;
-  if (g.dim == 1) {  // register 1D plans, tiles of 32..256 points, no ragged tile, <= 1024 problems
-    if (g.kernel_kind != K_REG1D || g.gen || g.ox != 0 || g.tx > 256 || g.nx % g.tx || g.ny > 1024) return false;
+  if (g.dim == 1) {  // register 1D plans (tiles of 32..1024 points), no ragged tile, <= 1024 problems
+    if (g.kernel_kind != K_REG1D || g.gen || g.ox != 0 || g.nx % g.tx || g.ny > 1024) return false;
     return (g.nx / g.tx) * g.ny <= 8LL * P->nsm;
   }
   // hierarchical register plans only: the classic comparison stays the paper's global-memory sweep

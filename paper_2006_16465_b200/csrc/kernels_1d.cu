@@ -564,7 +564,7 @@ cudaError_t launch_resident_1d(const Geom& g, void* X0, void* X1, const void* Q,
              : (wgt ? (const void*)res1d_kernel<float, CC, 2> : (const void*)res1d_kernel<float, CC, 0>);   \
     break;
   switch (g.tx / 32) {
-    HJ_R1(1) HJ_R1(2) HJ_R1(4) HJ_R1(8)
+    HJ_R1(1) HJ_R1(2) HJ_R1(4) HJ_R1(8) HJ_R1(16) HJ_R1(32)
     default: return cudaErrorInvalidValue;
   }
 #undef HJ_R1
