@@ -1,0 +1,79 @@
+"""The resident solver (res2d_kernel / res1d_kernel: the whole solve in one cooperative launch, tile
+iterates in registers across cycles) against the per-cycle path (HJ_RESIDENT=0): identical iterates,
+identical histories (the resident reduction replays rowsum_kernel + finalize_kernel's order) and
+identical cycle counts — and, through the existing parity suites, bitwise equal to the oracle."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2006_16465_b200 import hj
+from paper_2006_16465_b200.inputs import make_general, make_problem
+
+pytestmark = pytest.mark.gpu
+
+
+def _solve(p, env, **kw):
+    old = os.environ.get("HJ_RESIDENT")
+    try:
+        if env is None:
+            os.environ.pop("HJ_RESIDENT", None)
+        else:
+            os.environ["HJ_RESIDENT"] = env
+        return hj.jacobi_solve(p["dim"], p["nx"], p["ny"], p["h"], p["f"], p["bc"], p["x0"],
+                               stencil=p.get("stencil"), **kw)
+    finally:
+        if old is None:
+            os.environ.pop("HJ_RESIDENT", None)
+        else:
+            os.environ["HJ_RESIDENT"] = old
+
+
+CASES = [
+    ("R", 2, 64, 64, dict(tile=(32, 32), k=5, tol=0.0, max_cycles=9)),
+    ("P", 2, 256, 128, dict(tile=(32, 32), k=16, tol=1e-6, max_cycles=10**6)),
+    ("R", 2, 96, 160, dict(tile=(32, 32), k=3, tol=0.0, max_cycles=7, dtype="f32")),
+    ("M", 1, 256, 1, dict(tile=32, k=16, tol=1e-8, max_cycles=10**6)),
+    ("R", 1, 512, 4, dict(tile=64, k=7, tol=0.0, max_cycles=11)),
+    ("P", 1, 1 << 14, 1, dict(tile=1024, k=64, tol=1e-6, max_cycles=10**6)),
+    ("R", 1, 2048, 3, dict(tile=256, k=4, tol=0.0, max_cycles=5, dtype="f32")),
+]
+
+
+@pytest.mark.parametrize("proto,dim,nx,ny,kw", CASES)
+def test_resident_equals_per_cycle(proto, dim, nx, ny, kw):
+    p = make_problem(proto, dim, nx, ny) if (dim == 2 or ny == 1) else make_problem(proto, 1, nx, batch=ny)
+    a = _solve(p, None, mode="hier", **kw)
+    b = _solve(p, "0", mode="hier", **kw)
+    assert a["cycles"] == b["cycles"] and a["status"] == b["status"]
+    assert np.array_equal(a["x"], b["x"])
+    assert np.array_equal(a["history"], b["history"])
+
+
+def test_resident_general_coefficients_vs_oracle():
+    p = make_general("G", 2, 128, 96)
+    kw = dict(tile=(32, 32), k=6, tol=0.0, max_cycles=8)
+    a = _solve(p, None, mode="hier", **kw)
+    o = oracle.solve(2, 128, 96, p["h"], p["f"], p["bc"], p["x0"], stencil=p["stencil"], mode="hier", **kw)
+    assert np.array_equal(a["x"], o["x"])
+    np.testing.assert_allclose(a["history"], o["history"], rtol=1e-12, atol=0)
+
+
+def test_resident_resume_after_per_cycle_runs():
+    """plan.run (per-cycle launches) then plan.solve (resident) continues the same iteration."""
+    import torch
+    n = 128
+    p = make_problem("R", 2, n)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.as_tensor(a, device=dev)
+    plan = hj.Plan(2, n, n, p["h"], t(p["f"]), t(p["bc"]), t(p["x0"]), mode="hier", tile=(32, 32), k=4,
+                   tol=0.0, max_cycles=9)
+    plan.run(3)
+    r = plan.solve()
+    o = oracle.solve(2, n, n, p["h"], p["f"], p["bc"], p["x0"], mode="hier", tile=(32, 32), k=4, tol=0.0,
+                     max_cycles=9)
+    assert r["cycles"] == 9
+    assert np.array_equal(r["x"].cpu().numpy(), o["x"])
+    np.testing.assert_allclose(r["history"].cpu().numpy(), o["history"], rtol=1e-12, atol=0)
+    plan.close()
