@@ -171,7 +171,13 @@ hj_status hj_plan_reset(hj_plan *plan);
  * sum of their durations (the call then synchronises once, at the end). */
 hj_status hj_plan_run(hj_plan *plan, int64_t ncycles, float *kernel_ms);
 /* Run to convergence (or max_cycles) from the current state and fill result
- * (x and history are DEVICE pointers or NULL). */
+ * (x and history are DEVICE pointers or NULL).  Cycles run as CUDA graphs of G cycles with the
+ * stopping test on the device (host polls once per graph).  Single-GPU hierarchical plans small
+ * enough for one co-resident wave (2D: 32x32 tiles, nx and ny multiples of 32, at most 8 tiles per
+ * SM, no overlap; 1D: register tiles, no ragged tile, at most 1024 problems) instead run the whole
+ * solve in ONE cooperative launch with the tile iterates resident in registers — the same
+ * iterates, histories and cycle counts bit for bit; the environment variable HJ_RESIDENT=0 disables
+ * it (the same cycle). */
 hj_status hj_plan_solve(hj_plan *plan, hj_result *result);
 /* Number of launches of library kernels per cycle (for launch accounting). */
 int32_t hj_plan_launches_per_cycle(const hj_plan *plan);
