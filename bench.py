@@ -467,8 +467,9 @@ def main():
         fit = json.load(open(conv))["fit"]
         cyc = fit["hier_k16_o0"]["cycles_16384"]
         proj = {"tol": 1e-6, "measured": False, "cycles_projected": cyc, "seconds": cyc * ms_step * 1e-3,
-                "basis": "power-law fit of measured cycles-to-1e-6 at 1024^2..4096^2 (profiles/"
-                         "r01_convergence_scaling.json) x the measured cycle time"}
+                "basis": "power-law fit of measured cycles-to-1e-6 at 2048^2, 4096^2 and 8192^2 (8192^2: "
+                         "2,991,978 cycles, 1465 s measured; profiles/r01_convergence_scaling.json, "
+                         "r01_convergence_8192.json) x the measured cycle time"}
         if classic_ms:
             ccyc = fit["classic"]["cycles_16384"]
             proj["classic_sweeps_projected"] = ccyc
