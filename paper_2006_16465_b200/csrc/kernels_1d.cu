@@ -323,7 +323,7 @@ res1d_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, lo
     __syncthreads();
     if (warp == 0) {
       double S = 0.0;
-      for (int w = 0; w < 32; ++w) {
+      for (int w = 0; w < 32 && 32 * w < rows; ++w) {  // empty warps add +0.0: S unchanged
         const int g = 32 * w + lane;
         S += warp_sum(g < rows ? rsum[g] : 0.0);
       }
