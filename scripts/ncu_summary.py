@@ -87,6 +87,19 @@ def launches(csvpath, lines):
         v2 = sorted(v)
         lines.append(f"| `{k}` | {len(v)} | {v2[len(v2) // 2]:.1f} | {sum(v) / tot * 100:.1f}% |")
     lines.append("")
+    # the bench step itself (k = 16): cycle kernel + rowsum + finalize
+    import statistics as st
+    vals = []
+    for r in data:
+        vals.append((r[iK], float(r[iV].replace(",", "")) * scale.get(r[iU], 1)))
+    k16 = [v for k, v in vals if "reg2d_kernel" in k and v > 1500]
+    rs = [v for k, v in vals if "rowsum_kernel" in k]
+    fz = [v for k, v in vals if "finalize_kernel" in k]
+    if k16 and rs and fz:
+        a, b, c = st.median(k16), st.median(rs), st.median(fz)
+        lines.append(f"Bench step (k = 16; the launch list also holds the k = 1 / k = 4 load-store probes, the classic "
+                     f"comparison and the multigrid leg): cycle kernel {a:.1f} µs + rowsum {b:.1f} µs + finalize "
+                     f"{c:.1f} µs — the cycle kernel is {100 * a / (a + b + c):.1f}% of the step.\n")
 
 
 if __name__ == "__main__":
