@@ -25,6 +25,9 @@ cases = [
     (2, 127, 95, dict(mode="mg", tile=(32, 32), k=3, nu1=2, nu2=1, dtype="f32")),  # unfused correction
     (2, 63, 63, dict(mode="mg", tile=(8, 8), k=2, nu1=0, nu2=2)),        # smem levels, residual-only pass
     (1, 1023, 3, dict(mode="mg", tile=64, k=3)),                         # 1D multigrid
+    (2, 256, 128, dict(mode="hier", tile=(32, 32), k=6)),                # resident 2D (multi-CTA barrier)
+    (1, 256, 1, dict(mode="hier", tile=32, k=16)),                      # resident 1D, one CTA
+    (1, 4096, 2, dict(mode="hier", tile=128, k=5)),                     # resident 1D, multi-CTA
 ]
 for dim, nx, ny, kw in cases:
     p = make_problem("R", dim, nx, ny) if (dim == 2 or ny == 1) else make_problem("R", 1, nx, batch=ny)
