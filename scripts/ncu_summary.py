@@ -27,6 +27,9 @@ KEYS = [
     ("launch__grid_size", "grid size"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+     "shared-memory pipe utilisation % (LDS/STS + SHFL wavefronts)"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak (ncu)"),
     ("smsp__inst_executed_op_shfl.sum", "SHFL executed"),
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
 ]
