@@ -968,9 +968,11 @@ static bool resident_ok(const hj_plan* P) {
   const Geom& g = P->g;
   if (P->dist || P->peer || !P->mg.empty() || g.omega != 1.0) return false;
   if (const char* e = std::getenv("HJ_RESIDENT")) if (e[0] == '0') return false;
-  if (g.dim == 1) {  // register 1D plans (tiles of 32..1024 points), no ragged tile, <= 1024 problems
-    if (g.kernel_kind != K_REG1D || g.gen || g.ox != 0 || g.nx % g.tx || g.ny > 1024) return false;
-    return (g.nx / g.tx) * g.ny <= 8LL * P->nsm;
+  if (g.dim == 1) {  // register 1D plans (tiles of 32..1024 points), no ragged tile
+    if (g.kernel_kind != K_REG1D || g.gen || g.ox != 0 || g.nx % g.tx) return false;
+    const long long nt = (g.nx / g.tx) * g.ny;
+    if (nt <= 8LL * P->nsm && g.ny <= 1024) return true;            // one tile per warp (res1d)
+    return g.tx == 32 && nt <= 8LL * 32 * P->nsm && nt < (1LL << 31);  // up to 32 tiles per warp (res1dm)
   }
   // hierarchical register plans only: the classic comparison stays the paper's global-memory sweep
   if (!(g.kernel_kind == K_REG2D && g.tx == 32 && g.ty == 32 && g.ox == 0 && g.oy == 0)) return false;
@@ -982,15 +984,27 @@ static hj_status run_resident(hj_plan* P, bool* used) {
   const Geom& g = P->g;
   *used = false;
   const long long ntiles = g.dim == 2 ? (g.nx / 32) * (g.ny / 32) : (g.nx / g.tx) * g.ny;
+  const bool many = g.dim == 1 && !(ntiles <= 8LL * P->nsm && g.ny <= 1024);
+  if (many && !P->res_R) HJ_CUDA(cudaMalloc(&P->res_R, sizeof(double) * 2 * g.ny));
   if (!P->res_part) {
     HJ_CUDA(cudaMalloc(&P->res_part, sizeof(double) * 2 * ntiles));
     HJ_CUDA(cudaMalloc(&P->res_bar, 2 * sizeof(unsigned int)));
     HJ_CUDA(cudaMemsetAsync(P->res_bar, 0, 2 * sizeof(unsigned int), P->stream));
   }
   const int k = g.k;
-  cudaError_t e = (g.dim == 2 ? launch_resident_2d : launch_resident_1d)(
-      g, P->X[0], P->X[1], P->H2F, P->res_part, P->ctrl, P->hist, P->hist_cap, P->prm.tol,
-      (int)P->prm.tol_mode, P->prm.ref_residual, P->prm.max_cycles, k, P->res_bar, P->stream);
+  cudaError_t e;
+  if (many) {
+    // M <= 16: two CTAs per SM (<= 128 registers), M = 32: one
+    int M = 2;
+    while (M < 32 && ntiles > 8LL * M * (M <= 16 ? 2 : 1) * P->nsm) M *= 2;
+    e = launch_resident_1dm(g, M, P->X[0], P->X[1], P->H2F, P->res_part, P->res_R, P->ctrl, P->hist, P->hist_cap,
+                            P->prm.tol, (int)P->prm.tol_mode, P->prm.ref_residual, P->prm.max_cycles, k,
+                            P->res_bar, P->stream);
+  } else {
+    e = (g.dim == 2 ? launch_resident_2d : launch_resident_1d)(
+        g, P->X[0], P->X[1], P->H2F, P->res_part, P->ctrl, P->hist, P->hist_cap, P->prm.tol,
+        (int)P->prm.tol_mode, P->prm.ref_residual, P->prm.max_cycles, k, P->res_bar, P->stream);
+  }
   if (e == cudaErrorCooperativeLaunchTooLarge) {  // not co-resident here: the per-cycle path
     (void)cudaGetLastError();
     return HJ_OK;
@@ -1062,6 +1076,7 @@ void plan_free(hj_plan* P) {
   if (P->dist) dist_free(P);
   if (P->peer) peer_free(P);
   cudaFree(P->res_part);
+  cudaFree(P->res_R);
   cudaFree(P->res_bar);
   cudaFree(P->X[0]);
   cudaFree(P->X[1]);

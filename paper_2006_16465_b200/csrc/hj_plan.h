@@ -75,6 +75,7 @@ struct hj_plan {
   int mg_nu1 = 0, mg_nu2 = 0, mg_coarse = 0;
   // resident solver (launch_resident_2d): residual partials (2 x tiles) and the grid-barrier words
   double* res_part = nullptr;
+  double* res_R = nullptr;           // many-tile 1D variant: row sums (2 x rows)
   unsigned int* res_bar = nullptr;
 };
 

@@ -341,6 +341,138 @@ res1d_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, lo
 }
 
 // =============================================================================
+// RES1DM — the resident 1D solver for MANY small tiles (tiles of 32 points, e.g. the paper's
+// 1024 copies of N = 1024 with T = 32: 32,768 tiles): each warp owns M consecutive tiles for the
+// whole solve, lane l holding point l of each, so a sub-iteration is M independent shuffle+update
+// chains (latency hidden by ILP across tiles).  Per cycle: the tiles' frozen halo values (lane 0:
+// left, lane 31: right; L2 loads), fused residual, k sub-iterations, x_{c+1} stored, per-tile
+// partials; grid barrier; the row sums of rowsum_kernel, distributed over the CTAs; grid
+// barrier; every CTA replays finalize_kernel's reduction (warps in parallel, the 32 warp sums in
+// order) and takes the same hj_decide decision.  Bitwise the per-cycle path's iterates and
+// histories.
+// =============================================================================
+template <typename T, int M, int SK>
+__global__ void __launch_bounds__(256, (M <= 16 ? 2 : 1))
+res1dm_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, long long pitch,
+              long long fpitch, int ntpr, int rows, double* __restrict__ part, double* __restrict__ R,
+              Ctrl* __restrict__ ctrl, double* __restrict__ hist, long long hist_cap, double rdiv, double tol,
+              int tol_mode, double ref_residual, long long max_cycles, int k, double omd, unsigned int* bar) {
+  constexpr int COL0 = 16 / sizeof(T);
+  __shared__ Ctrl cs;
+  __shared__ int s_done;
+  __shared__ double ws[32];
+  __shared__ long long s_off[8][M];       // interior point 0 of each of my tiles in X
+  __shared__ T s_h[8][M][2];              // the tiles' frozen halo values (left, right)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = ntpr * rows;
+  const int tb = (blockIdx.x * 8 + warp) * M;  // my first tile
+  const T om = (T)omd;
+  if (threadIdx.x == 0) {
+    cs = *ctrl;
+    s_done = cs.done;
+  }
+  for (int m = lane; m < M; m += 32) {
+    const int t = tb + m < ntiles ? tb + m : 0;
+    s_off[warp][m] = (long long)(t / ntpr) * pitch + COL0 + (long long)(t % ntpr) * 32;
+  }
+  __syncthreads();
+  if (s_done) return;
+  T x[M], q[M];
+  int p = (int)(cs.c & 1);
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int t = tb + m;
+    const long long o = s_off[warp][m];
+    const long long qo = (long long)((t < ntiles ? t : 0) / ntpr) * fpitch + (long long)((t < ntiles ? t : 0) % ntpr) * 32;
+    x[m] = (t < ntiles) ? (p ? X1 : X0)[o + lane] : T(0);
+    q[m] = (t < ntiles) ? Q[qo + lane] : T(0);
+  }
+  for (;;) {
+    const T* Xc = p ? X1 : X0;
+    T* Xn = p ? X0 : X1;
+    const long long c = cs.c;
+    const int kk = c >= max_cycles ? 0 : k;
+    double* pc = part + (c & 1) * (long long)ntiles;
+    double* Rc = R + (c & 1) * (long long)rows;
+    // frozen halos of x_c: lane m of the warp fetches tile m's two values (L2)
+    for (int m = lane; m < M; m += 32) {
+      if (tb + m < ntiles) {
+        const long long o = s_off[warp][m];
+        s_h[warp][m][0] = __ldcg(Xc + o - 1);
+        s_h[warp][m][1] = __ldcg(Xc + o + 32);
+      }
+    }
+    __syncwarp();
+    // fused residual of the snapshot (reg1d_tile's expression), per-tile partials
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      T l = __shfl_up_sync(FULL, x[m], 1);
+      T r = __shfl_down_sync(FULL, x[m], 1);
+      if (lane == 0) l = s_h[warp][m][0];
+      if (lane == 31) r = s_h[warp][m][1];
+      const double s = res1((double)x[m], (double)l, (double)r, (double)(T(2) * q[m]));
+      const double v = warp_sum(__fma_rn(s, s, 0.0));
+      if (lane == 0 && tb + m < ntiles) pc[tb + m] = v;
+    }
+#pragma unroll 1
+    for (int s = 0; s < kk; ++s) {
+      constexpr int G = M < 4 ? M : 4;  // tiles per group: all shuffles of a group issued first
+#pragma unroll
+      for (int m0 = 0; m0 < M; m0 += G) {
+        T l[G], r[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          l[g] = __shfl_up_sync(FULL, x[m0 + g], 1);
+          r[g] = __shfl_down_sync(FULL, x[m0 + g], 1);
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const T hv = s_h[warp][m0 + g][lane == 31 ? 1 : 0];
+          if (lane == 0) l[g] = hv;
+          if (lane == 31) r[g] = hv;
+          T nv = upd1(l[g], r[g], q[m0 + g]);
+          if constexpr (SK == 2) nv = damp(om, x[m0 + g], nv);
+          x[m0 + g] = nv;
+        }
+      }
+    }
+    if (kk > 0) {
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+        if (tb + m < ntiles) Xn[s_off[warp][m] + lane] = x[m];
+    }
+    grid_barrier(bar, gridDim.x);
+    // rowsum_kernel's row sums, rows spread over the grid's warps
+    for (int g = blockIdx.x * 8 + warp; g < rows; g += gridDim.x * 8) {
+      double v = 0.0;
+      for (int qq = lane; qq < ntpr; qq += 32) v += __ldcg(pc + (long long)g * ntpr + qq);
+      v = warp_sum(v);
+      if (lane == 0) Rc[g] = v;
+    }
+    grid_barrier(bar, gridDim.x);
+    // finalize_kernel's reduction: warp w of its 1024 threads sums rows 32w + lane (+1024 ...)
+    for (int w = warp; w < 32; w += 8) {
+      double v = 0.0;
+      for (int i = 32 * w + lane; i < rows; i += 1024) v += __ldcg(Rc + i);
+      v = warp_sum(v);
+      if (lane == 0) ws[w] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double S = 0.0;
+      for (int w = 0; w < 32; ++w) S += ws[w];
+      hj_decide(&cs, S, blockIdx.x == 0 ? hist : nullptr, hist_cap, rdiv, tol, tol_mode, ref_residual,
+                max_cycles);
+      s_done = cs.done;
+    }
+    __syncthreads();
+    if (s_done) break;
+    p ^= 1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ctrl = cs;
+}
+
+// =============================================================================
 // SMEM1D — the paper's Appendix A design: blockDim.x = T threads, shared memory
 // [container 0 (T+2) | container 1 (T+2) | rhs (T)], __syncthreads per
 // sub-iteration, write-back of the latest container (reading c8), into the other global
@@ -545,6 +677,31 @@ cudaError_t configure_1d() {
   HJ_CFG(float)
 #undef HJ_CFG
   return cudaSuccess;
+}
+
+// Many-tile variant (tiles of 32 points, M tiles per warp); R: 2 x rows doubles.
+cudaError_t launch_resident_1dm(const Geom& g, int M, void* X0, void* X1, const void* Q, double* part, double* R,
+                                Ctrl* ctrl, double* hist, long long hist_cap, double tol, int tol_mode,
+                                double ref_residual, long long max_cycles, int k, unsigned int* bar, cudaStream_t st) {
+  int ntpr = (int)(g.nx / 32), rows = (int)g.ny;
+  long long pitch = g.pitch, fpitch = g.fpitch;
+  double rdiv = g.rdiv, om = g.omega;
+  void* args[] = {&X0, &X1, &Q, &pitch, &fpitch, &ntpr, &rows, &part, &R, &ctrl, &hist, &hist_cap, &rdiv, &tol,
+                  &tol_mode, &ref_residual, &max_cycles, &k, &om, &bar};
+  const long long ntiles = (long long)ntpr * rows;
+  const dim3 grid((unsigned)((ntiles + 8LL * M - 1) / (8LL * M))), block(256);
+  const bool f64 = g.dtype == HJ_F64;
+  const void* fn = nullptr;
+#define HJ_RM(MM)                                                                                  \
+  case MM:                                                                                         \
+    fn = f64 ? (const void*)res1dm_kernel<double, MM, 0> : (const void*)res1dm_kernel<float, MM, 0>; \
+    break;
+  switch (M) {
+    HJ_RM(2) HJ_RM(4) HJ_RM(8) HJ_RM(16) HJ_RM(32)
+    default: return cudaErrorInvalidValue;
+  }
+#undef HJ_RM
+  return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, st);
 }
 
 cudaError_t launch_resident_1d(const Geom& g, void* X0, void* X1, const void* Q, double* part, Ctrl* ctrl,

@@ -17,10 +17,10 @@ out = {}
 for dim, n, mode, k, tol, proto in ((2, 1024, "hier", 16, 1e-4, "P"), (2, 1024, "hier", 16, 1e-6, "P"),
                                     (2, 512, "hier", 8, 1e-6, "P"), (1, 256, "hier", 16, 1e-8, "M"),
                                     (1, 256, "hier", 16, 1e-8, "P"), (1, 1024, "hier", 16, 1e-6, "P"),
-                                    (1, 1 << 20, "hier", 64, 1e-4, "P")):
-    p = make_problem(proto, dim, n)
+                                    (1, 1 << 20, "hier", 64, 1e-4, "P"), (1, 1024, "hier", 16, 1e-4, "B")):
+    p = make_problem("P", 1, n, batch=1024) if proto == "B" else make_problem(proto, dim, n)
     t = {kk: torch.from_numpy(p[kk]).to(dev) for kk in ("f", "bc", "x0")}
-    args = (dim, p["nx"], p["ny"], p["h"], t["f"], t["bc"], t["x0"])
+    args = (p["dim"], p["nx"], p["ny"], p["h"], t["f"], t["bc"], t["x0"])
     kw = dict(mode=mode, tile=(32, 32) if dim == 2 else (1024 if n >= 1 << 20 else 32), k=k, tol=tol,
               max_cycles=10**8, history=False)
     hj.jacobi_solve_device(*args, **kw)

@@ -38,6 +38,9 @@ CASES = [
     ("R", 1, 512, 4, dict(tile=64, k=7, tol=0.0, max_cycles=11)),
     ("P", 1, 1 << 14, 1, dict(tile=1024, k=64, tol=1e-6, max_cycles=10**6)),
     ("R", 1, 2048, 3, dict(tile=256, k=4, tol=0.0, max_cycles=5, dtype="f32")),
+    ("R", 1, 1024, 300, dict(tile=32, k=5, tol=0.0, max_cycles=6)),            # many tiles per warp
+    ("P", 1, 1024, 1024, dict(tile=32, k=16, tol=1e-4, max_cycles=10**6)),   # the paper's 1D workload
+    ("R", 1, 4096, 1500, dict(tile=32, k=3, tol=0.0, max_cycles=4, dtype="f32")),
 ]
 
 
