@@ -791,7 +791,7 @@ static hj_status launch_vcycle(hj_plan* P, bool timed) {
   const long long INF = LLONG_MAX;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
-    while (P->evpool.size() < 2 * (P->evused + 1)) {
+    while (P->evpool.size() < 2 * size_t(P->evused + 1)) {
       cudaEvent_t ev;
       HJ_CUDA(cudaEventCreate(&ev));
       P->evpool.push_back(ev);
@@ -859,7 +859,7 @@ hj_status launch_cycle(hj_plan* P, int p, bool timed, float* acc_ms) {
   (void)acc_ms;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timed) {
-    while (P->evpool.size() < 2 * (P->evused + 1)) {
+    while (P->evpool.size() < 2 * size_t(P->evused + 1)) {
       cudaEvent_t ev;
       HJ_CUDA(cudaEventCreate(&ev));
       P->evpool.push_back(ev);
