@@ -190,10 +190,14 @@ def multigrid_leg(dev, stream):
     prm = dict(mode="mg", tile=(TILE, TILE), k=4, nu1=1, nu2=1, max_cycles=200)
     plan = hj.Plan(2, n, n, h, f, bc, x0, stream=stream, tol=1e-6, **prm)
     plan.solve(history=False)
-    plan.reset()
-    r = plan.solve(history=True)
+    secs = []
+    for _ in range(3):  # three timed solves from x0 (graphs instantiated by the warm solve)
+        plan.reset()
+        r = plan.solve(history=True)
+        secs.append(r["seconds_solve"])
     hist = r["history"].cpu().tolist()
     plan.close()
+    secs.sort()
     tp = hj.Plan(2, n, n, h, f, bc, x0, stream=stream, tol=0.0, **prm)
     tp.run(2)
     vc_ms = tp.run(10, timed=True) / 10
@@ -219,7 +223,8 @@ def multigrid_leg(dev, stream):
     return {"tol": 1e-6, "grid": n, "protocol": "P (f=1, x0=1, g=0)", "measured": True,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                          "algorithmic_bytes_per_vcycle": vb},
-            "vcycles": r["cycles"], "converged": r["converged"], "seconds": r["seconds_solve"],
+            "vcycles": r["cycles"], "converged": r["converged"], "seconds": secs[1],
+            "seconds_min": secs[0], "seconds_max": secs[2], "repeats": 3,
             "ms_per_vcycle": vc_ms, "launches_per_vcycle": lpc,
             "final_rel_residual": hist[-1] / hist[0],
             "method": "V(1,1) multigrid, hierarchical 32x32 k=4 damped-Jacobi smoother (omega 4/5), "
