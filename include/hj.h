@@ -79,8 +79,9 @@ typedef enum {
                            interpolation, mg_coarse_cycles plain hierarchical cycles on the
                            coarsest grid).  One "cycle" = one V-cycle; the stopping test and
                            history are those of the other modes.  Poisson only (stencil NULL),
-                           overlap 0, no row slabs; nx (and ny in 2D) odd >= 3; every level
-                           uses tile = min(tile, n_level) and k sub-iterations.               */
+                           overlap 0, no row slabs; nx (and ny in 2D) odd >= 3; every level,
+                           the finest included, uses tile = min(tile, n_level) and k
+                           sub-iterations.                                                    */
 } hj_mode;
 typedef enum { HJ_TOL_RELATIVE = 0, HJ_TOL_ABSOLUTE = 1 } hj_tol_mode;
 typedef enum {

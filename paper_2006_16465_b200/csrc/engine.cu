@@ -325,9 +325,10 @@ hj_status validate(const hj_problem* pb, const hj_params* pr, bool need_f) {
     return HJ_OK;
   }
   if (pr->k < 1) { set_error("k must be >= 1"); return HJ_ERR_INVALID_CONFIG; }
-  if (pr->tile_x < 1 || pr->tile_x > pb->nx) { set_error("tile_x must be in [1, nx]"); return HJ_ERR_INVALID_CONFIG; }
+  const bool mg = pr->mode == HJ_MULTIGRID;  // multigrid clips the tile to every level (c24)
+  if (pr->tile_x < 1 || (!mg && pr->tile_x > pb->nx)) { set_error("tile_x must be in [1, nx]"); return HJ_ERR_INVALID_CONFIG; }
   if (pb->dim == 1 && pr->tile_y != 1) { set_error("dim 1 needs tile_y == 1"); return HJ_ERR_INVALID_CONFIG; }
-  if (pb->dim == 2 && (pr->tile_y < 1 || pr->tile_y > pb->ny)) { set_error("tile_y must be in [1, ny]"); return HJ_ERR_INVALID_CONFIG; }
+  if (pb->dim == 2 && (pr->tile_y < 1 || (!mg && pr->tile_y > pb->ny))) { set_error("tile_y must be in [1, ny]"); return HJ_ERR_INVALID_CONFIG; }
   return HJ_OK;
 }
 
@@ -437,6 +438,13 @@ static int kernels_per_smooth(const hj_plan* L) {
 // ------------------------------------------------------------------ plans ---
 hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st, const DistInfo* di,
                      hj_plan** out) {
+  hj_params prc;
+  if (pr && pb && pr->mode == HJ_MULTIGRID) {  // reading c24: every level, the finest included, uses
+    prc = *pr;                                 // tile = min(tile, n_level)
+    if (prc.tile_x > pb->nx) prc.tile_x = (int32_t)pb->nx;
+    if (pb->dim == 2 && prc.tile_y > pb->ny) prc.tile_y = (int32_t)pb->ny;
+    pr = &prc;
+  }
   HJ_TRY(validate(pb, pr, true));
   int nsm = 0;
   HJ_TRY(ensure_configured(&nsm));
