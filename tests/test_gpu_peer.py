@@ -85,3 +85,10 @@ def test_peer_transport_bitwise_vs_single_gpu(case, nranks):
             assert np.array_equal(r["x2"].reshape(r["re"] - r["rb"], case["nx"]), xr[r["rb"]:r["re"]])
     # cycle kernel(s) (+ halo kernel unless fused into the register kernel) + rowsum + finalize
     assert res[0]["lpc"] >= 3
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["name"] in ("reg2d_R_fixed", "reg2d_ragged_x_fused_halo")],
+                         ids=["reg2d_R_fixed", "reg2d_ragged_x_fused_halo"])
+def test_peer_transport_four_ranks(case):
+    """Four ranks: two interior ranks exchange with both neighbours."""
+    test_peer_transport_bitwise_vs_single_gpu(case, 4)
