@@ -120,3 +120,11 @@ def test_mg_full_size_bitwise_bench_config():
     # (n - 1) eps (Higham, Accuracy and Stability, Thm 4.1 with positive terms), i.e. n eps / 2 for
     # the norm (reading c15).  Measured: 1.2e-10 at n = 2.7e8 (the 1e-12 bar holds below ~1e4 cells).
     assert_parity(o, g, hist_rtol=n * n * np.finfo(np.float64).eps / 2)
+
+
+def test_mg_full_size_f32_bitwise():
+    """fp32 multigrid at full size (16383^2): one V-cycle, every cell bitwise equal to the oracle."""
+    n = 16383
+    p = make_problem("R", 2, n)
+    o, g = both(p, cycles=1, tile=(32, 32), k=4, nu1=1, nu2=1, dtype="f32")
+    assert_parity(o, g, hist_rtol=n * n * np.finfo(np.float64).eps / 2)
