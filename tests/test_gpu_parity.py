@@ -263,6 +263,21 @@ def test_full_size_sampled_tiles(n, proto, dtype):
         del d, xg
 
 
+def test_full_size_full_grid_one_cycle_bench_config():
+    """The bench's exact launch configuration (16384^2, protocol P, 32x32 register kernel, k = 16):
+    after one cycle EVERY cell equals the oracle's full-grid cycle (the oracle needs ~10 GB of host
+    memory and ~15 s), and after two cycles too."""
+    n = 16384
+    p = make_problem("P", 2, n)
+    for cycles in (1, 2):
+        o, g = both(p, cycles=cycles, mode="hier", tile=(32, 32), k=16)
+        assert g["cycles"] == o["cycles"] == cycles
+        assert np.array_equal(g["x"], o["x"])
+        # residual history: sequential oracle sum vs tile tree (reading c15; recursive-sum bound)
+        np.testing.assert_allclose(g["history"], o["history"], rtol=n * n * np.finfo(np.float64).eps / 2, atol=0)
+        del o, g
+
+
 def test_dist_path_single_rank_matches_single_gpu():
     """jacobi_solve_dist with one rank (1-rank NCCL communicator, rowpart_local + allreduce path,
     NCCL inside the graph-captured cycle) reproduces the single-GPU solve bit for bit."""
