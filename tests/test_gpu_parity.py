@@ -276,6 +276,9 @@ def test_full_size_full_grid_one_cycle_bench_config():
         # residual history: sequential oracle sum vs tile tree (reading c15; recursive-sum bound)
         np.testing.assert_allclose(g["history"], o["history"], rtol=n * n * np.finfo(np.float64).eps / 2, atol=0)
         del o, g
+    # the classic comparison sweep at the same size
+    o, g = both(p, cycles=2, mode="classic")
+    assert np.array_equal(g["x"], o["x"])
 
 
 def test_dist_path_single_rank_matches_single_gpu():
