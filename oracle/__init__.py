@@ -12,10 +12,12 @@ follows in ``hjo.cpp``.
 Parity status: pinned by tests/test_oracle_pins.py against
 closed forms (cos(pi h) decay, discrete exact solutions, direct solves,
 brute-force dense cycle matrices, the paper's printed resource figures) —
-except the exact iterates of the hierarchical schedule with k>1 on many tiles,
-which have no closed form and are pinned only through limits (k=1, one tile),
-brute force at tiny sizes, structure (halo locality, order independence) and
-cross-implementation cycle counts.
+and, for the exact iterates of the hierarchical schedule with k>1 on many tiles
+(no closed form), through limits (k=1, one tile), brute force at tiny sizes, an
+independent vectorised NumPy re-implementation matched bit for bit
+(tests/test_oracle_vectorized.py), structure (halo locality, order independence)
+and cross-implementation cycle counts.  The multigrid V-cycle is pinned in
+tests/test_oracle_mg.py.
 """
 from __future__ import annotations
 
