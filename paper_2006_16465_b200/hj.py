@@ -3,8 +3,10 @@
 Every step of the solve runs in the CUDA kernels of libhj.so; there is no Python or CPU
 fallback: if the library is missing or no sm_100 device is usable, calls raise.
 Names follow the C-ABI: ``jacobi_solve``, ``jacobi_solve_device``, ``jacobi_solve_dist``,
-``hj_resource_figures``, ``hj_nccl_unique_id``, ``hj_last_error`` and the ``Plan`` wrapper
-of ``hj_plan_*``.
+``hj_resource_figures``, ``hj_nccl_unique_id``, ``hj_last_error`` and the ``Plan`` wrappers of
+``hj_plan_*`` (``Plan``; ``DistPlan`` for NCCL row slabs; ``PeerPlan`` for row slabs over the
+peer-memory transport).  ``mode``: "hier" (the paper's hierarchical cycle), "classic" (global-
+memory Jacobi), "mg" (multigrid V-cycles with the hierarchical cycle as smoother).
 """
 from __future__ import annotations
 
