@@ -275,21 +275,32 @@ __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ 
   // c16) and for residual-only cycles; fp64 folds it into the first sub-iteration below.
   constexpr bool FOLD = sizeof(T) == 8;
   double acc = 0.0;
-  if (!FOLD || kk == 0) acc = tl.residual(lx, ly);
   int s = 0;
-  if (FOLD && kk > 0) {
+  if (FOLD && kk >= 8 && ((kk - 1) & 1)) {
+    // even k >= 8: the residual sweep and the next plain sweep in ONE basic block with the warp
+    // reduction of the residual after both, so ptxas interleaves its dependent shuffle chain
+    // with the plain sweep instead of exposing it (the same value: warp_sum of the same a4)
     double a4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent accumulation chains
     tl.template sweep_mo<true>(lx, ly, a4);
-    acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-    s = 1;
-  }
-  acc = warp_sum(acc);
-  if (lane == 0) part[t] = acc;
-  // remaining sub-iterations, halo frozen
-  if (s < kk && ((kk - s) & 1)) {
     tl.template sweep_mo<false>(lx, ly);
-    ++s;
+    acc = warp_sum((a4[0] + a4[1]) + (a4[2] + a4[3]));
+    s = 2;
+  } else {
+    if (!FOLD || kk == 0) acc = tl.residual(lx, ly);
+    if (FOLD && kk > 0) {
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};
+      tl.template sweep_mo<true>(lx, ly, a4);
+      acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      s = 1;
+    }
+    acc = warp_sum(acc);
+    if (s < kk && ((kk - s) & 1)) {
+      tl.template sweep_mo<false>(lx, ly);
+      ++s;
+    }
   }
+  if (lane == 0) part[t] = acc;
+  // remaining sub-iterations (an even number), halo frozen
 #pragma unroll 1
   for (; s < kk; s += 2) {
     tl.template sweep_mo<false>(lx, ly);
