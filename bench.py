@@ -114,13 +114,22 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def ncu_traffic():
-    """dram bytes per launch of the cycle kernel from the committed ncu --set full summary."""
+def ncu_traffic(n, k, mode, cells_local):
+    """dram bytes per launch of the cycle kernel from the committed ncu --set full summary (one
+    16384^2, k = 16 hierarchical launch on one GPU).  Only for that configuration; a row slab's
+    launch (N > 1) gets the figure scaled by its share of the cells (stated in traffic_basis)."""
     p = os.path.join(ROOT, "profiles", "ncu_cycle_kernel.json")
-    if os.path.exists(p):
-        d = json.load(open(p))
-        return d.get("dram_bytes_per_launch")
-    return None
+    if not (os.path.exists(p) and n == N_GRID and k == K_SUB and mode == "hier"):
+        return None, None
+    d = json.load(open(p))
+    full = d.get("dram_bytes_per_launch")
+    if full is None:
+        return None, None
+    share = cells_local / float(n * n)
+    basis = f"ncu --set full, one {n}^2 launch ({d.get('round', '?')})"
+    if share < 1.0:
+        basis += f", scaled to this rank's slab ({share:.4f} of the cells)"
+    return full * share, basis
 
 
 def cpu_oracle_sample(n_cells_side, k, cycles):
@@ -480,6 +489,7 @@ def main():
             proj["classic_sweeps_projected"] = ccyc
             proj["classic_seconds"] = ccyc * classic_ms * 1e-3
             proj["speedup_vs_classic"] = proj["classic_seconds"] / proj["seconds"]
+    traffic, traffic_basis = ncu_traffic(n, k, args.mode, cells_local)
     out = {"metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -491,7 +501,8 @@ def main():
                             + (", no flush needed" if 3 * 8 * n * n / world > 4 * 126e6 else
                                " (L2-resident: not an HBM measurement)")},
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                        "frac": achieved / peak, "traffic": ncu_traffic(), "peak_source": peak_src,
+                        "frac": achieved / peak, "traffic": traffic, "traffic_basis": traffic_basis,
+                        "peak_source": peak_src,
                         "kernel_ms": kern_ms, "bytes_per_cell": BYTES_PER_CELL,
                         "classic_sweep_ms": classic_ms,
                         "load_store_phase": ls_phase,

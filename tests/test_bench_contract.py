@@ -22,3 +22,21 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert "workload" in d["config"]
+
+
+def test_ncu_traffic_scales_to_the_rank_slab():
+    """roofline.traffic is the committed ncu figure of one full 16384^2 launch; a row slab's launch
+    (N > 1) reports its share of it, other configurations report none."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    full = json.load(open(os.path.join(ROOT, "profiles", "ncu_cycle_kernel.json")))["dram_bytes_per_launch"]
+    n = b.N_GRID
+    t1, basis1 = b.ncu_traffic(n, b.K_SUB, "hier", n * n)
+    assert t1 == full and "scaled" not in basis1
+    t2, basis2 = b.ncu_traffic(n, b.K_SUB, "hier", n * n // 2)
+    assert t2 == full / 2 and "scaled" in basis2
+    assert b.ncu_traffic(2048, b.K_SUB, "hier", 2048 * 2048) == (None, None)
+    assert b.ncu_traffic(n, 4, "hier", n * n) == (None, None)
+    assert b.ncu_traffic(n, b.K_SUB, "classic", n * n) == (None, None)
