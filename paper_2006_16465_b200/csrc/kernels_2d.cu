@@ -279,7 +279,8 @@ __device__ __forceinline__ void reg2d_tile(const Wt2& wt, const T* __restrict__ 
   if (FOLD && kk >= 8 && ((kk - 1) & 1)) {
     // even k >= 8: the residual sweep and the next plain sweep in ONE basic block with the warp
     // reduction of the residual after both, so ptxas interleaves its dependent shuffle chain
-    // with the plain sweep instead of exposing it (the same value: warp_sum of the same a4)
+    // with the plain sweep instead of exposing it (the same value: warp_sum of the same a4).
+    // Below k = 8 the HBM-bound cycle measured faster in the old order.
     double a4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent accumulation chains
     tl.template sweep_mo<true>(lx, ly, a4);
     tl.template sweep_mo<false>(lx, ly);
