@@ -30,7 +30,9 @@
  *    means g = 0 (the paper's u = 0).
  *  - x0 NULL means a zero initial guess (the paper's protocol passes ones).
  *  - Iterates are kept in hj_params.dtype (f64 or f32); the residual is always accumulated in
- *    f64 from s = h^2 f - (stencil applied to x) (h^2-scaled form, reported unscaled).
+ *    f64 from s = h2f - (stencil applied to x) (h^2-scaled form, reported unscaled), where
+ *    h2f = h^2 f for f64 and h2f = (double)(float)(h*h*f), the right-hand side the fp32 iteration
+ *    actually solves, for f32 (reading c16; pinned in tests/test_oracle_pins.py).
  *  - Ownership: every input pointer is borrowed for the duration of the call only; every
  *    output buffer is caller-allocated; the library allocates and frees its own device
  *    scratch (two padded iterate buffers, the h^2 f array, residual partials, history).
@@ -139,8 +141,11 @@ typedef struct {
 
 typedef struct {
   double *x;               /* caller-allocated nx*ny doubles (f64 even for f32 solves)       */
-  double *history;         /* caller-allocated max_cycles+1 doubles or NULL;
-                              history[c] = ||f - A x_c||_2 for c = 0..cycles                  */
+  double *history;         /* caller-allocated hj_history_capacity(params) doubles (=
+                              max_cycles+1 up to 2^24) or NULL; history[c] = ||f - A x_c||_2
+                              for c = 0..min(cycles, capacity-1).  jacobi_solve*, with history,
+                              reject max_cycles+1 > capacity (HJ_ERR_INVALID_CONFIG);
+                              hj_plan_solve truncates (never writes past capacity)            */
   int64_t cycles;          /* first c at which the test held (0 if x0 already satisfies it)  */
   int32_t converged;
   double initial_residual; /* ||f - A x0||_2                                                  */
@@ -180,6 +185,10 @@ hj_status hj_plan_run(hj_plan *plan, int64_t ncycles, float *kernel_ms);
  * iterates, histories and cycle counts bit for bit; the environment variable HJ_RESIDENT=0 disables
  * it (the same cycle). */
 hj_status hj_plan_solve(hj_plan *plan, hj_result *result);
+/* Entries of the residual history kept for these parameters: min(max_cycles + 1, 2^24) (the
+ * environment variable HJ_HIST_CAP lowers the 2^24 limit, for tests).  The history buffer of
+ * hj_plan_solve must hold this many doubles; 0 for params == NULL. */
+int64_t hj_history_capacity(const hj_params *params);
 /* Number of launches of library kernels per cycle (for launch accounting). */
 int32_t hj_plan_launches_per_cycle(const hj_plan *plan);
 hj_status hj_plan_destroy(hj_plan *plan);

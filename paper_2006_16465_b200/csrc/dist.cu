@@ -173,7 +173,10 @@ hj_status jacobi_solve_dist(const hj_problem* pb, const hj_params* pr, hj_result
   if (!dist || !res || !res->x || !dist->nccl_id) { set_error("NULL argument"); return HJ_ERR_INVALID_ARG; }
   HJ_TRY(validate_dist(pb, pr, dist));
   const long long rb = dist->row_begin, re = dist->row_end;
-  if (res->history && pr->max_cycles + 1 > HIST_CAP) { set_error("history too long"); return HJ_ERR_INVALID_CONFIG; }
+  if (res->history && history_capacity(pr->max_cycles) < pr->max_cycles + 1) {
+    set_error("history is limited to 2^24 cycles (HJ_HIST_CAP); pass history = NULL");
+    return HJ_ERR_INVALID_CONFIG;
+  }
   const long long nloc = pb->nx * (re - rb);
   const long long nbc = 2 * pb->nx + 2 * pb->ny;
   double *f = nullptr, *bc = nullptr, *x0 = nullptr, *x = nullptr, *hist = nullptr;
@@ -203,7 +206,7 @@ hj_status jacobi_solve_dist(const hj_problem* pb, const hj_params* pr, hj_result
     DCK(cudaMemcpyAsync(x0, pb->x0, sizeof(double) * nloc, cudaMemcpyHostToDevice, st));
   }
   DCK(cudaMalloc(&x, sizeof(double) * nloc));
-  if (res->history) DCK(cudaMalloc(&hist, sizeof(double) * (pr->max_cycles + 1)));
+  if (res->history) DCK(cudaMalloc(&hist, sizeof(double) * history_capacity(pr->max_cycles)));
   hj_problem dp = *pb;
   dp.f = f;
   dp.bc = bc;
@@ -220,7 +223,7 @@ hj_status jacobi_solve_dist(const hj_problem* pb, const hj_params* pr, hj_result
   plan_free(P);
   if (s == HJ_OK || s == HJ_NOT_CONVERGED || s == HJ_ERR_NUMERIC) {
     DCK(cudaMemcpyAsync(hx, x, sizeof(double) * nloc, cudaMemcpyDeviceToHost, st));
-    if (hh) DCK(cudaMemcpyAsync(hh, hist, sizeof(double) * (res->cycles + 1), cudaMemcpyDeviceToHost, st));
+    if (hh) DCK(cudaMemcpyAsync(hh, hist, sizeof(double) * lmin(res->cycles + 1, history_capacity(pr->max_cycles)), cudaMemcpyDeviceToHost, st));
     DCK(cudaStreamSynchronize(st));
   }
 #undef DCK

@@ -29,6 +29,15 @@ namespace hj {
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 
+long long history_limit() {
+  static const long long lim = [] {
+    const char* e = std::getenv("HJ_HIST_CAP");
+    const long long v = e ? std::atoll(e) : 0;
+    return v > 0 && v < HIST_CAP ? v : HIST_CAP;
+  }();
+  return lim;
+}
+
 cudaError_t configure_2d();
 cudaError_t configure_1d();
 
@@ -246,27 +255,36 @@ hj_status make_tmap(CUtensorMap* tm, const void* base, int dtype, uint64_t d0, u
 
 long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
 
+// Per device: the SM count and the large-dynamic-shared-memory opt-ins (cudaFuncSetAttribute is
+// per device), done once for each device a plan is created on.
 hj_status ensure_configured(int* nsm) {
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  static int sms = 0;
-  std::call_once(once, [] {
-    int dev = 0;
-    err = cudaGetDevice(&dev);
-    if (err == cudaSuccess) {
+  constexpr int MAXDEV = 64;
+  static std::mutex mu;
+  static bool done[MAXDEV] = {};
+  static cudaError_t err[MAXDEV] = {};
+  static int sms[MAXDEV] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess && (dev < 0 || dev >= MAXDEV)) e = cudaErrorInvalidDevice;
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done[dev]) {
       cudaDeviceProp prop;
-      err = cudaGetDeviceProperties(&prop, dev);
-      if (err == cudaSuccess && prop.major < 10) err = cudaErrorInvalidDevice;
-      sms = prop.multiProcessorCount;
+      cudaError_t r = cudaGetDeviceProperties(&prop, dev);
+      if (r == cudaSuccess && prop.major < 10) r = cudaErrorInvalidDevice;
+      if (r == cudaSuccess) sms[dev] = prop.multiProcessorCount;
+      if (r == cudaSuccess) r = configure_2d();
+      if (r == cudaSuccess) r = configure_1d();
+      err[dev] = r;
+      done[dev] = true;
     }
-    if (err == cudaSuccess) err = configure_2d();
-    if (err == cudaSuccess) err = configure_1d();
-  });
-  if (err != cudaSuccess) {
-    set_error(std::string("libhj: no usable sm_100 device: ") + cudaGetErrorString(err));
+    e = err[dev];
+  }
+  if (e != cudaSuccess) {
+    set_error(std::string("libhj: no usable sm_100 device: ") + cudaGetErrorString(e));
     return HJ_ERR_CUDA;
   }
-  *nsm = sms;
+  *nsm = sms[dev];
   return HJ_OK;
 }
 
@@ -340,8 +358,12 @@ static hj_status choose_kernel(const hj_problem* pb, const hj_params* pr, int* k
     // TMA box origins must be 16-byte aligned along x: with overlapping blocks every block start
     // b*(32-o) and the shifted last start nx-32 must be a multiple of 16/sizeof(T) elements.
     const long long al = 16 / (long long)esz;
-    const bool aligned = pr->overlap == 0 || ((32 - pr->overlap) % al == 0 && (pb->nx - 32) % al == 0);
-    if (pr->kernel == HJ_KERNEL_AUTO && pr->tile_x == 32 && pr->tile_y == 32 && aligned) {
+    const int ox = pr->overlap, oy = pr->overlap_y < 0 ? pr->overlap : pr->overlap_y;
+    const bool aligned = ox == 0 || ((32 - ox) % al == 0 && (pb->nx - 32) % al == 0);
+    // with overlap on either axis the register kernel runs EVERY block as a full 32x32 tile, so an
+    // axis without overlap must have no ragged tile (its ragged tiles would need the edge kernel)
+    const bool full = (ox == 0 && oy == 0) || ((ox > 0 || pb->nx % 32 == 0) && (oy > 0 || pb->ny % 32 == 0));
+    if (pr->kernel == HJ_KERNEL_AUTO && pr->tile_x == 32 && pr->tile_y == 32 && aligned && full) {
       *kind = K_REG2D;
       return HJ_OK;
     }
@@ -537,7 +559,7 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
   P->stream = st;
   P->ny_global = ny_global;
   P->gy0 = gy0;
-  P->hist_cap = pr->max_cycles + 1 < HIST_CAP ? pr->max_cycles + 1 : HIST_CAP;
+  P->hist_cap = history_capacity(pr->max_cycles);
   const size_t xbytes = size_t(g.pitch) * g.rows * esz;
   const size_t fbytes = size_t(g.fpitch) * g.frows * esz;
   auto fail = [&](hj_status e) { plan_free(P); return e; };
@@ -1065,7 +1087,9 @@ hj_status plan_solve(hj_plan* P, hj_result* res, double* x_dev, double* hist_dev
       extract_kernel<float><<<blocks, 256, 0, st>>>((const float*)X, g.pitch, g.dim, g.nx, g.ny, (int)g.col0, x_dev);
     HJ_CUDA(cudaGetLastError());
   }
-  if (hist_dev) HJ_CUDA(cudaMemcpyAsync(hist_dev, P->hist, sizeof(double) * (cd + 1), cudaMemcpyDeviceToDevice, st));
+  // the history holds min(cycles + 1, hist_cap) entries (truncated past the cap, never beyond it)
+  if (hist_dev)
+    HJ_CUDA(cudaMemcpyAsync(hist_dev, P->hist, sizeof(double) * lmin(cd + 1, P->hist_cap), cudaMemcpyDeviceToDevice, st));
   HJ_CUDA(cudaStreamSynchronize(st));
   res->cycles = cd;
   res->converged = c.converged;
@@ -1160,6 +1184,7 @@ hj_status hj_plan_solve(hj_plan* P, hj_result* res) {
   if (!P || !res) { set_error("NULL argument"); return HJ_ERR_INVALID_ARG; }
   return plan_solve(P, res, res->x, res->history);
 }
+int64_t hj_history_capacity(const hj_params* pr) { return pr ? history_capacity(pr->max_cycles) : 0; }
 int32_t hj_plan_launches_per_cycle(const hj_plan* P) { return P ? launches_per_cycle(P) : 0; }
 hj_status hj_plan_destroy(hj_plan* P) {
   plan_free(P);
@@ -1168,6 +1193,10 @@ hj_status hj_plan_destroy(hj_plan* P) {
 
 hj_status jacobi_solve_device(const hj_problem* pb, const hj_params* pr, hj_result* res, void* stream) {
   if (!res) { set_error("NULL result"); return HJ_ERR_INVALID_ARG; }
+  if (res->history && pr && history_capacity(pr->max_cycles) < pr->max_cycles + 1) {
+    set_error("history is limited to 2^24 cycles (HJ_HIST_CAP); pass history = NULL");
+    return HJ_ERR_INVALID_CONFIG;
+  }
   auto t0 = std::chrono::steady_clock::now();
   hj_plan* P = nullptr;
   HJ_TRY(plan_build(pb, pr, (cudaStream_t)stream, nullptr, &P));
@@ -1180,8 +1209,8 @@ hj_status jacobi_solve_device(const hj_problem* pb, const hj_params* pr, hj_resu
 hj_status jacobi_solve(const hj_problem* pb, const hj_params* pr, hj_result* res) {
   if (!res || !res->x) { set_error("NULL result or result->x"); return HJ_ERR_INVALID_ARG; }
   HJ_TRY(validate(pb, pr, true));
-  if (res->history && pr->max_cycles + 1 > HIST_CAP) {
-    set_error("history is limited to 2^24 cycles; pass history = NULL");
+  if (res->history && history_capacity(pr->max_cycles) < pr->max_cycles + 1) {
+    set_error("history is limited to 2^24 cycles (HJ_HIST_CAP); pass history = NULL");
     return HJ_ERR_INVALID_CONFIG;
   }
   auto t0 = std::chrono::steady_clock::now();
@@ -1215,7 +1244,7 @@ hj_status jacobi_solve(const hj_problem* pb, const hj_params* pr, hj_result* res
     SCK(cudaMemcpyAsync(x0, pb->x0, sizeof(double) * n, cudaMemcpyHostToDevice, st));
   }
   SCK(cudaMalloc(&x, sizeof(double) * n));
-  if (res->history) SCK(cudaMalloc(&hist, sizeof(double) * (pr->max_cycles + 1)));
+  if (res->history) SCK(cudaMalloc(&hist, sizeof(double) * history_capacity(pr->max_cycles)));
   hj_problem dp = *pb;
   dp.f = f;
   dp.bc = bc;
@@ -1231,7 +1260,7 @@ hj_status jacobi_solve(const hj_problem* pb, const hj_params* pr, hj_result* res
   plan_free(P);
   if (s == HJ_OK || s == HJ_NOT_CONVERGED || s == HJ_ERR_NUMERIC) {
     SCK(cudaMemcpyAsync(hx, x, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-    if (hh) SCK(cudaMemcpyAsync(hh, hist, sizeof(double) * (res->cycles + 1), cudaMemcpyDeviceToHost, st));
+    if (hh) SCK(cudaMemcpyAsync(hh, hist, sizeof(double) * lmin(res->cycles + 1, history_capacity(pr->max_cycles)), cudaMemcpyDeviceToHost, st));
     SCK(cudaStreamSynchronize(st));
   }
 #undef SCK

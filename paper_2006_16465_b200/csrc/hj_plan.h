@@ -82,6 +82,14 @@ struct hj_plan {
 namespace hj {
 
 constexpr long long HIST_CAP = 1LL << 24;
+// Entries of the residual history a plan keeps: 2^24, or HJ_HIST_CAP from the environment (tests
+// lower it to cross the cap in a few hundred cycles).  history_capacity(max_cycles) =
+// min(max_cycles + 1, limit) without overflow.
+long long history_limit();
+inline long long history_capacity(long long max_cycles) {
+  const long long lim = history_limit();
+  return max_cycles >= lim - 1 ? lim : max_cycles + 1;
+}
 
 hj_status validate(const hj_problem* pb, const hj_params* pr, bool need_f);
 hj_status validate_dist(const hj_problem* pb, const hj_params* pr, const hj_dist* dist);

@@ -19,9 +19,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhj.so")
 
 HJ_OK, HJ_NOT_CONVERGED, HJ_ERR_INVALID_ARG, HJ_ERR_INVALID_CONFIG = 0, 1, 2, 3
-HJ_ERR_NUMERIC, HJ_ERR_CUDA, HJ_ERR_NCCL, HJ_ERR_OOM = 4, 5, 6, 7
+HJ_ERR_NUMERIC, HJ_ERR_CUDA, HJ_ERR_NCCL, HJ_ERR_OOM, HJ_ERR_PEER = 4, 5, 6, 7, 8
 STATUS_NAMES = {0: "HJ_OK", 1: "HJ_NOT_CONVERGED", 2: "HJ_ERR_INVALID_ARG", 3: "HJ_ERR_INVALID_CONFIG",
-                4: "HJ_ERR_NUMERIC", 5: "HJ_ERR_CUDA", 6: "HJ_ERR_NCCL", 7: "HJ_ERR_OOM"}
+                4: "HJ_ERR_NUMERIC", 5: "HJ_ERR_CUDA", 6: "HJ_ERR_NCCL", 7: "HJ_ERR_OOM", 8: "HJ_ERR_PEER"}
 MODES = {"hier": 0, "hierarchical": 0, "classic": 1, "mg": 2, "multigrid": 2}
 DTYPES = {"f64": 0, "float64": 0, "f32": 1, "float32": 1}
 TOL_MODES = {"rel": 0, "relative": 0, "abs": 1, "absolute": 1}
@@ -108,10 +108,17 @@ def lib():
             fn.restype = ctypes.c_int
         L.hj_last_error.restype = ctypes.c_char_p
         L.hj_last_error.argtypes = []
+        L.hj_history_capacity.restype = ctypes.c_int64
+        L.hj_history_capacity.argtypes = [ctypes.POINTER(hj_params)]
         L.hj_plan_launches_per_cycle.restype = ctypes.c_int32
         L.hj_plan_launches_per_cycle.argtypes = [_P]
         _lib = L
     return _lib
+
+
+def history_capacity(prm) -> int:
+    """hj_history_capacity: entries of the residual history a solve with these params keeps."""
+    return int(lib().hj_history_capacity(ctypes.byref(prm)))
 
 
 def hj_last_error() -> str:
@@ -161,7 +168,7 @@ def jacobi_solve(dim, nx, ny, h, f, bc=None, x0=None, *, history=True, stencil=N
     stencil = _host(stencil, _nstencil(dim, nx, ny), "stencil")
     prm = make_params(**params)
     x = np.empty(n)
-    hist = np.empty(prm.max_cycles + 1) if history else None
+    hist = np.empty(history_capacity(prm)) if history else None
     pb = hj_problem(dim, nx, ny, float(h), _hp(f), _hp(bc), _hp(x0), _hp(stencil))
     res = hj_result(x.ctypes.data, _hp(hist), 0, 0, 0.0, 0.0, 0.0, 0.0)
     st = _check(lib().jacobi_solve(ctypes.byref(pb), ctypes.byref(prm), ctypes.byref(res)),
@@ -187,7 +194,7 @@ def jacobi_solve_device(dim, nx, ny, h, f, bc=None, x0=None, *, history=True, st
     prm = make_params(**params)
     dev = f.device
     x = torch.empty(nx * ny, dtype=torch.float64, device=dev)
-    hist = torch.empty(prm.max_cycles + 1, dtype=torch.float64, device=dev) if history else None
+    hist = torch.empty(history_capacity(prm), dtype=torch.float64, device=dev) if history else None
     pb = hj_problem(dim, nx, ny, float(h), _dptr(f), _dptr(bc), _dptr(x0), _dptr(stencil))
     res = hj_result(_dptr(x), _dptr(hist), 0, 0, 0.0, 0.0, 0.0, 0.0)
     s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
@@ -222,7 +229,7 @@ def jacobi_solve_dist(nx, ny, h, f_local, bc, x0_local, *, rank, nranks, nccl_id
     stencil = _host(stencil, 5, "stencil")
     prm = make_params(**params)
     x = np.empty(nloc)
-    hist = np.empty(prm.max_cycles + 1) if history else None
+    hist = np.empty(history_capacity(prm)) if history else None
     pb = hj_problem(2, nx, ny, float(h), _hp(f), _hp(bc), _hp(x0), _hp(stencil))
     res = hj_result(x.ctypes.data, _hp(hist), 0, 0, 0.0, 0.0, 0.0, 0.0)
     idbuf = ctypes.create_string_buffer(nccl_id, 128)
@@ -267,12 +274,14 @@ class Plan:
         import torch
         dev = self._keep[0].device
         x = torch.empty(self.nx * self.ny, dtype=torch.float64, device=dev)
-        hist = torch.empty(min(self.prm.max_cycles + 1, 1 << 24), dtype=torch.float64, device=dev) if history else None
+        cap = history_capacity(self.prm)
+        hist = torch.empty(cap, dtype=torch.float64, device=dev) if history else None
         res = hj_result(_dptr(x), _dptr(hist), 0, 0, 0.0, 0.0, 0.0, 0.0)
         st = _check(lib().hj_plan_solve(self._p, ctypes.byref(res)),
                     ok=(HJ_OK, HJ_NOT_CONVERGED, HJ_ERR_NUMERIC))
-        return _result(res, st, x.view(self.ny, self.nx) if self.dim == 2 else x,
-                       None if hist is None else hist[: res.cycles + 1])
+        # the history is truncated at the capacity (include/hj.h)
+        return _result(res, st, x.view(self.ny, self.nx) if self.dim == 2 or self.ny > 1 else x,
+                       None if hist is None else hist[: min(res.cycles + 1, cap)])
 
     def launches_per_cycle(self):
         return lib().hj_plan_launches_per_cycle(self._p)

@@ -10,6 +10,7 @@ import pytest
 import oracle
 from paper_2006_16465_b200 import hj
 from paper_2006_16465_b200.inputs import make_problem
+from tests import _exact
 
 pytestmark = pytest.mark.gpu
 
@@ -269,11 +270,18 @@ def test_full_size_full_grid_one_cycle_bench_config():
     memory and ~15 s), and after two cycles too."""
     n = 16384
     p = make_problem("P", 2, n)
+    xs = [p["x0"]]
     for cycles in (1, 2):
         o, g = both(p, cycles=cycles, mode="hier", tile=(32, 32), k=16)
         assert g["cycles"] == o["cycles"] == cycles
         assert np.array_equal(g["x"], o["x"])
-        # residual history: sequential oracle sum vs tile tree (reading c15; recursive-sum bound)
+        xs.append(g["x"])
+        # residual history: the GPU's tile tree to 1e-12 of the exactly summed definition evaluated
+        # on the (bit-identical) iterates x_0 .. x_c (tests/_exact.py; VERDICT r1 weak #3) ...
+        for c in range(cycles + 1):
+            want = _exact.residual_2d(n, n, p["h"], p["f"], p["bc"], xs[c])
+            assert abs(g["history"][c] - want) <= 1e-12 * want, (c, g["history"][c], want)
+        # ... and the oracle's naive sequential sum within its recursive-summation bound (reading c15)
         np.testing.assert_allclose(g["history"], o["history"], rtol=n * n * np.finfo(np.float64).eps / 2, atol=0)
         del o, g
     # the classic comparison sweep at the same size

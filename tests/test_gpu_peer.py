@@ -3,13 +3,17 @@ sharing the one GPU of this box (CUDA IPC works between processes on the same de
 refuses duplicate GPUs, so this is the only multi-rank data-path test that runs here).
 
 Bar (DESIGN.md §9, c18): every rank's rows, the history and the cycle count are bitwise equal to
-the single-GPU solve of the same problem."""
+the single-GPU solve of the same problem, and — the parity gate itself — every rank's rows are
+bitwise equal to the CPU oracle's iterate, the history within 1e-12 of the oracle's and the cycle
+count exactly the oracle's (VERDICT r1 weak #2)."""
+import functools
 import multiprocessing as mp
 import os
 
 import numpy as np
 import pytest
 
+import oracle
 from paper_2006_16465_b200 import hj
 from paper_2006_16465_b200.inputs import make_general, make_problem
 
@@ -56,6 +60,18 @@ def _single(case):
     return hj.jacobi_solve(2, nx, ny, p["h"], p["f"], p["bc"], p["x0"], stencil=p.get("stencil"), **prm)
 
 
+@functools.lru_cache(maxsize=None)
+def _oracle_cached(name):
+    case = next(c for c in CASES if c["name"] == name)
+    nx, ny = case["nx"], case["ny"]
+    p = make_general(case["recipe"], 2, nx, ny) if case.get("general") else make_problem(case["recipe"], 2, nx, ny)
+    prm = dict(mode=case["mode"], tile=case["tile"], k=case["k"], tol=case["tol"], max_cycles=case["max_cycles"],
+               dtype=case.get("dtype", "f64"))
+    if case["mode"] == "classic":
+        prm["k"] = 1
+    return oracle.solve(2, nx, ny, p["h"], p["f"], p["bc"], p["x0"], stencil=p.get("stencil"), **prm)
+
+
 CASES = [
     dict(name="reg2d_R_fixed", recipe="R", nx=128, ny=192, mode="hier", tile=(32, 32), k=5, tol=0.0, max_cycles=7),
     dict(name="reg2d_ragged_x_fused_halo", recipe="R", nx=100, ny=128, mode="hier", tile=(32, 32), k=5, tol=0.0,
@@ -74,8 +90,15 @@ CASES = [
 def test_peer_transport_bitwise_vs_single_gpu(case, nranks):
     ref = _single(case)
     res = _run(case, nranks)
+    o = _oracle_cached(case["name"])
     xr = np.asarray(ref["x"]).reshape(case["ny"], case["nx"])
+    xo = np.asarray(o["x"]).reshape(case["ny"], case["nx"])
     for r in res:
+        # against the oracle (the parity gate) ...
+        assert r["cycles"] == o["cycles"]
+        assert np.array_equal(r["x"].reshape(r["re"] - r["rb"], case["nx"]), xo[r["rb"]:r["re"]])
+        np.testing.assert_allclose(r["hist"], o["history"], rtol=1e-12, atol=0)
+        # ... and bitwise against the one-GPU solve (P-invariance, c18)
         assert r["status"] == ref["status"]
         assert r["cycles"] == ref["cycles"]
         assert np.array_equal(r["x"].reshape(r["re"] - r["rb"], case["nx"]), xr[r["rb"]:r["re"]])

@@ -335,3 +335,42 @@ def test_batched_1d_rows_are_independent_problems():
                          k=k, tol=1e-4, max_cycles=10**6, history=False)
         assert a["cycles"] == s["cycles"]
     assert oracle.resource_figures(1, 1024, 1024, 32)[0] == 1024 * 32   # PAPER.md:215 block count
+
+
+@pytest.mark.parametrize("dim,nx,ny,tile,k", [(2, 48, 40, (16, 16), 3), (1, 200, 1, (32, 1), 5)])
+def test_fp32_residual_is_that_of_the_rounded_system(dim, nx, ny, tile, k):
+    """Reading c16 pinned: the fp32 history[c] is ||b32 - A x_c||_2 where x_c is
+    the fp32 iterate, A the textbook Poisson matrix (assembled here with scipy, h^2-scaled) and b32 the
+    right-hand side the fp32 iteration solves — float(h^2 f) and the ring float(g) — evaluated as a
+    sparse matrix-vector product and an exactly rounded sum (math.fsum), to 1e-12.  The true-rhs reading
+    (||f - A x_c|| with h^2 f and g in double) differs by far more than that, so the pin tells them apart."""
+    p = make_problem("R", dim, nx, ny)
+    h = p["h"]
+    A = _brute.poisson_matrix(dim, nx, ny)
+
+    def rhs(f, bc):
+        r = f.copy()
+        if dim == 1:
+            r[0] += bc[0]
+            r[-1] += bc[1]
+        else:
+            r = r.reshape(ny, nx)
+            r[0, :] += bc[:nx]
+            r[-1, :] += bc[nx:2 * nx]
+            r[:, 0] += bc[2 * nx:2 * nx + ny]
+            r[:, -1] += bc[2 * nx + ny:]
+            r = r.reshape(-1)
+        return r
+
+    r32 = lambda a: np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+    b32 = rhs(r32((h * h) * p["f"]), r32(p["bc"]))        # the system the fp32 iteration solves
+    b64 = rhs((h * h) * p["f"], p["bc"])                  # the true system
+    norm = lambda v: math.sqrt(math.fsum((v * v).tolist())) / (h * h)
+    for c in (0, 1, 2, 5):
+        r = run(p, mode="hier", dtype="f32", tile=tile, k=k, tol=0.0, max_cycles=c)
+        x = r["x"].reshape(-1)
+        assert np.array_equal(x, r32(x))                  # the iterate is an fp32 vector
+        want = norm(b32 - A @ x)
+        assert abs(r["history"][c] - want) <= 1e-12 * want, (c, r["history"][c], want)
+        other = norm(b64 - A @ x)
+        assert abs(other - want) > 10e-12 * want           # the pin discriminates the two readings (> 10x its bar)
