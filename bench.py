@@ -240,6 +240,75 @@ def multigrid_leg(dev, stream):
                       "full weighting, bilinear interpolation (SURVEY 8(f) NEXT #4, DESIGN.md c24)"}
 
 
+def multi_rank_parity(rank, world, dev, stream, one_gpu, n=2048, cycles=2, k=K_SUB):
+    """N > 1 self-check (VERDICT r1 next #1d): on a small random grid (protocol R, non-zero ring) each
+    rank solves its row slab for `cycles` cycles with EACH transport, the slabs are gathered on rank 0
+    and compared bit for bit with rank 0's one-GPU solve of the whole grid AND with the CPU oracle
+    (the parity gate), histories to 1e-12.  NCCL cannot run with several ranks on one GPU (the
+    HJ_BENCH_ONE_GPU testing mode); it is then reported as skipped."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2006_16465_b200 import hj
+    from paper_2006_16465_b200.inputs import make_problem
+    from paper_2006_16465_b200.slabs import slab
+    p = make_problem("R", 2, n)
+    rb, re = slab(n, TILE, rank, world)
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
+    f = t(p["f"].reshape(n, n)[rb:re].reshape(-1))
+    x0 = t(p["x0"].reshape(n, n)[rb:re].reshape(-1))
+    bc = t(p["bc"])
+    prm = dict(mode="hier", tile=(TILE, TILE), k=k, tol=0.0, max_cycles=cycles)
+    res = {}
+    for tr in ("peer", "nccl"):
+        if tr == "nccl" and one_gpu:
+            res[tr] = "skipped (ranks share one GPU: NCCL refuses duplicate devices)"
+            continue
+        try:
+            if tr == "peer":
+                pl = hj.PeerPlan(n, n, p["h"], f, bc, x0, rank=rank, nranks=world, row_begin=rb, row_end=re,
+                                 stream=stream, **prm)
+                pl.connect()
+            else:
+                idb = [hj.hj_nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(idb, src=0)
+                pl = hj.DistPlan(n, n, p["h"], f, bc, x0, rank=rank, nranks=world, nccl_id=idb[0], row_begin=rb,
+                                 row_end=re, stream=stream, **prm)
+            r = pl.solve(history=True)
+            mine = (rb, r["x"].cpu().numpy(), r["history"].cpu().numpy(), r["cycles"])
+            pl.close()
+        except Exception as e:  # noqa: BLE001 - every rank reports; rank 0 records the failure
+            mine = ("error", f"{type(e).__name__}: {e}")
+        allv = [None] * world if rank == 0 else None
+        dist.gather_object(mine, allv, dst=0)
+        if rank != 0:
+            continue
+        errs = [a[1] for a in allv if a[0] == "error"]
+        if errs:
+            res[tr] = {"ok": False, "error": errs[0][:300]}
+            continue
+        x = np.concatenate([a[1].reshape(-1, n) for a in sorted(allv, key=lambda a: a[0])])
+        hists = [a[2] for a in allv]
+        res[tr] = {"x": x, "hist": hists, "cycles": [a[3] for a in allv]}
+    if rank != 0:
+        return None
+    import oracle
+    o = oracle.solve(2, n, n, p["h"], p["f"], p["bc"], p["x0"], **prm)
+    one = hj.jacobi_solve(2, n, n, p["h"], p["f"], p["bc"], p["x0"], **prm)
+    out = {"grid": n, "cycles": cycles, "k": k, "inputs": "protocol R (random f, x0, ring)",
+           "against": "CPU oracle (bitwise iterate, history 1e-12) and rank 0's one-GPU solve (bitwise)"}
+    for tr, v in res.items():
+        if not isinstance(v, dict) or "x" not in v:
+            out[tr] = v
+            continue
+        ok_o = bool(np.array_equal(v["x"], o["x"])) and all(
+            np.allclose(h, o["history"], rtol=1e-12, atol=0) for h in v["hist"]) and all(
+            c == o["cycles"] for c in v["cycles"])
+        ok_1 = bool(np.array_equal(v["x"], one["x"])) and all(np.array_equal(h, one["history"]) for h in v["hist"])
+        out[tr] = ok_o and ok_1
+    return out
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -326,6 +395,9 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # N > 1: the data path of BOTH transports proved against the oracle before anything is timed
+    parity = multi_rank_parity(rank, world, dev, stream, one_gpu) if world > 1 else None
+
     # warm-up (also instantiates graphs / events)
     plan.run(args.warmup, timed=True)
     barrier()
@@ -347,6 +419,32 @@ def main():
     value = n * n * k / (ms_step * 1e-3)
 
     plan.close()
+
+    # N > 1 with the peer transport as the headline: the NCCL transport (grouped send/recv halos +
+    # allreduce of the residual row sums, north star) timed the same way as a second key
+    nccl_leg = None
+    if world > 1 and transport and transport.startswith("peer") and not one_gpu:
+        try:
+            idn = [hj.hj_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(idn, src=0)
+            npl = hj.DistPlan(n, n, h, f, bc, x0, rank=rank, nranks=world, nccl_id=idn[0], row_begin=rb,
+                              row_end=re, stream=stream, **prm)
+            npl.run(args.warmup, timed=True)
+            barrier()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(sobj)
+            nk = npl.run(args.steps, timed=True)
+            a1.record(sobj)
+            barrier()
+            tn = torch.tensor([a0.elapsed_time(a1), nk], dtype=torch.float64, device=dev)
+            allreduce(tn, dist.ReduceOp.MAX)
+            nms = tn[0].item() / args.steps
+            nccl_leg = {"transport": "nccl (send/recv halos + allreduce)", "ms_per_step": nms,
+                        "value": n * n * k / (nms * 1e-3), "kernel_ms": tn[1].item() / args.steps,
+                        "launches_per_cycle": npl.launches_per_cycle()}
+            npl.close()
+        except Exception as e:  # noqa: BLE001 - keep the headline line
+            nccl_leg = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     # the classic global-memory sweep on the same grid (comparison for the time-to-tol projection)
     classic_ms = None
@@ -514,6 +612,9 @@ def main():
            "time_to_tol": ttt,
            "time_to_1e-6": proj,
            "time_to_1e-6_multigrid": mg}
+    if world > 1:
+        out["parity_check"] = parity
+        out["nccl_transport"] = nccl_leg
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -31,3 +31,8 @@ def test_bench_two_ranks_one_gpu():
     assert d["gpu_launches"] > 0
     assert d["roofline"]["bound"] == "hbm" and d["roofline"]["traffic"] is None  # not the ncu config
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    # the N > 1 self-check: both transports' slabs vs the oracle and the one-GPU solve (NCCL cannot run
+    # with two ranks on one GPU and reports itself skipped)
+    pc = d["parity_check"]
+    assert pc["peer"] is True, pc
+    assert isinstance(pc["nccl"], str) and pc["nccl"].startswith("skipped")
