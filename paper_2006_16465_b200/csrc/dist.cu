@@ -36,6 +36,7 @@ struct NcclApi {
   decltype(&ncclGroupEnd) GroupEnd = nullptr;
   decltype(&ncclAllReduce) AllReduce = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  decltype(&ncclCommGetAsyncError) CommGetAsyncError = nullptr;
   bool ok = false;
   std::string err;
 };
@@ -50,7 +51,7 @@ const NcclApi& nccl() {
     if (!h) { api.err = dlerror(); return; }
 #define HJ_SYM(name) api.name = reinterpret_cast<decltype(api.name)>(dlsym(h, "nccl" #name)); if (!api.name) { api.err = "missing nccl" #name; return; }
     HJ_SYM(GetUniqueId) HJ_SYM(CommInitRank) HJ_SYM(CommDestroy) HJ_SYM(Send) HJ_SYM(Recv)
-    HJ_SYM(GroupStart) HJ_SYM(GroupEnd) HJ_SYM(AllReduce) HJ_SYM(GetErrorString)
+    HJ_SYM(GroupStart) HJ_SYM(GroupEnd) HJ_SYM(AllReduce) HJ_SYM(GetErrorString) HJ_SYM(CommGetAsyncError)
 #undef HJ_SYM
     api.ok = true;
   });
@@ -61,6 +62,11 @@ const NcclApi& nccl() {
 struct DistState {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
+  // overlapped exchange (REG2D plans without edge tiles, nranks > 1): the halo group runs on its
+  // own stream, forked after the boundary tile rows and joined before the next cycle
+  bool overlap = false;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
 };
 
 namespace hj {
@@ -107,6 +113,31 @@ hj_status dist_create(hj_plan* P, const DistInfo* di) {
   ncclUniqueId id;
   std::memcpy(&id, di->nccl_id, sizeof(id));
   HJ_NCCL(CommInitRank(&d->comm, di->nranks, id, di->rank));
+  const Geom& g = P->g;
+  const char* env = std::getenv("HJ_NCCL_OVERLAP");
+  d->overlap = d->nranks > 1 && g.kernel_kind == K_REG2D && !g.ox && !g.oy && g.nx % 32 == 0 &&
+               g.ny % 32 == 0 && g.ny / 32 >= 3 && !(env && env[0] == '0');
+  if (d->overlap) {
+    HJ_CUDA(cudaStreamCreateWithFlags(&d->cs, cudaStreamNonBlocking));
+    HJ_CUDA(cudaEventCreateWithFlags(&d->ev_bnd, cudaEventDisableTiming));
+    HJ_CUDA(cudaEventCreateWithFlags(&d->ev_halo, cudaEventDisableTiming));
+  }
+  return HJ_OK;
+}
+
+bool dist_overlap(const hj_plan* P) { return P->dist && P->dist->overlap; }
+
+// Surface an asynchronous NCCL failure (a peer died, a network error) as HJ_ERR_NCCL instead of a
+// hang: polled by the host between cycle graphs.
+hj_status dist_check(hj_plan* P) {
+  DistState* d = P->dist;
+  if (!d || !d->comm || d->nranks == 1) return HJ_OK;
+  ncclResult_t ae = ncclSuccess;
+  HJ_NCCL(CommGetAsyncError(d->comm, &ae));
+  if (ae != ncclSuccess && ae != ncclInProgress) {
+    set_error(std::string("NCCL asynchronous error: ") + nccl().GetErrorString(ae));
+    return HJ_ERR_NCCL;
+  }
   return HJ_OK;
 }
 
@@ -132,6 +163,26 @@ hj_status dist_halo_exchange(hj_plan* P, int buf) {
   return HJ_OK;
 }
 
+// Overlapped form: fork the halo group onto the comm stream once the boundary tile rows (the only
+// writers of rows 1 and R) are done; join_halo makes the plan's stream wait for it (before anything
+// reads the ghost rows: the next cycle).  Both are graph-capturable (event fork / join).
+hj_status dist_halo_fork(hj_plan* P, int buf) {
+  DistState* d = P->dist;
+  HJ_CUDA(cudaEventRecord(d->ev_bnd, P->stream));
+  HJ_CUDA(cudaStreamWaitEvent(d->cs, d->ev_bnd, 0));
+  cudaStream_t main = P->stream;
+  P->stream = d->cs;
+  const hj_status s = dist_halo_exchange(P, buf);
+  P->stream = main;
+  HJ_TRY(s);
+  HJ_CUDA(cudaEventRecord(d->ev_halo, d->cs));
+  return HJ_OK;
+}
+hj_status dist_halo_join(hj_plan* P) {
+  HJ_CUDA(cudaStreamWaitEvent(P->stream, P->dist->ev_halo, 0));
+  return HJ_OK;
+}
+
 hj_status dist_initial_exchange(hj_plan* P) { return dist_halo_exchange(P, 0); }
 
 hj_status dist_allreduce(hj_plan* P) {
@@ -148,6 +199,12 @@ hj_status dist_allreduce(hj_plan* P) {
 
 void dist_free(hj_plan* P) {
   if (!P->dist) return;
+  if (P->dist->cs) {
+    cudaStreamSynchronize(P->dist->cs);
+    cudaStreamDestroy(P->dist->cs);
+  }
+  if (P->dist->ev_bnd) cudaEventDestroy(P->dist->ev_bnd);
+  if (P->dist->ev_halo) cudaEventDestroy(P->dist->ev_halo);
   if (P->dist->comm && nccl().ok) nccl().CommDestroy(P->dist->comm);
   delete P->dist;
   P->dist = nullptr;

@@ -21,6 +21,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "hj_internal.cuh"
 #include "hj_plan.h"
 
@@ -28,6 +30,13 @@ namespace hj {
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+// NVTX ranges around the host-side phases (plan build, runs, solves, graph capture) so one nsys trace
+// shows them next to the kernels and the NCCL streams.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 long long history_limit() {
   static const long long lim = [] {
@@ -460,6 +469,7 @@ static int kernels_per_smooth(const hj_plan* L) {
 // ------------------------------------------------------------------ plans ---
 hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st, const DistInfo* di,
                      hj_plan** out) {
+  NvtxRange nv("hj_plan_build");
   hj_params prc;
   if (pr && pb && pr->mode == HJ_MULTIGRID) {  // reading c24: every level, the finest included, uses
     prc = *pr;                                 // tile = min(tile, n_level)
@@ -689,6 +699,7 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
 }
 
 hj_status plan_reset(hj_plan* P) {
+  NvtxRange nv("hj_plan_reset");
   const Geom& g = P->g;
   cudaStream_t st = P->stream;
   const int blocks = 4 * P->nsm;
@@ -899,13 +910,28 @@ hj_status launch_cycle(hj_plan* P, int p, bool timed, float* acc_ms) {
     P->evused++;
     HJ_CUDA(cudaEventRecord(e0, st));
   }
-  cudaError_t e = g.dim == 2 ? launch_cycle_2d(g, a, P->nsm, st) : launch_cycle_1d(g, a, P->nsm, st);
+  const bool ovl = dist_overlap(P);
+  cudaError_t e;
+  if (ovl) {
+    // overlapped NCCL transport: the slab's boundary tile rows first, their rows sent
+    // on the comm stream while the interior tile rows run, joined before the next cycle
+    const int nty = (int)(g.ny / 32);
+    a.ty0 = 0; a.tys = nty - 1; a.nty_run = 2;
+    e = launch_cycle_2d(g, a, P->nsm, st);
+    if (e == cudaSuccess) {
+      HJ_TRY(dist_halo_fork(P, p ^ 1));
+      a.ty0 = 1; a.tys = 1; a.nty_run = nty - 2;
+      e = launch_cycle_2d(g, a, P->nsm, st);
+    }
+  } else {
+    e = g.dim == 2 ? launch_cycle_2d(g, a, P->nsm, st) : launch_cycle_1d(g, a, P->nsm, st);
+  }
   if (e != cudaSuccess) {
     set_error(std::string("cycle kernel launch: ") + cudaGetErrorString(e));
     return HJ_ERR_CUDA;
   }
   if (timed) HJ_CUDA(cudaEventRecord(e1, st));
-  if (P->dist) HJ_TRY(dist_halo_exchange(P, p ^ 1));
+  if (P->dist && !ovl) HJ_TRY(dist_halo_exchange(P, p ^ 1));
   PeerDsts pd{};
   PeerSync ps{};
   if (P->peer) {
@@ -921,6 +947,7 @@ hj_status launch_cycle(hj_plan* P, int p, bool timed, float* acc_ms) {
                                       P->prm.tol, (int)P->prm.tol_mode, P->prm.ref_residual,
                                       P->prm.max_cycles, ps, P->rp_stride);
   HJ_CUDA(cudaGetLastError());
+  if (ovl) HJ_TRY(dist_halo_join(P));
   return HJ_OK;
 }
 
@@ -939,6 +966,7 @@ static hj_status drain_events(hj_plan* P, float* acc) {
 static hj_status get_graph(hj_plan* P, int G, cudaGraphExec_t* out) {
   auto it = P->graphs.find(G);
   if (it != P->graphs.end()) { *out = it->second; return HJ_OK; }
+  NvtxRange nv("hj_graph_capture");
   cudaGraph_t graph;
   HJ_CUDA(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
   hj_status s = HJ_OK;
@@ -956,6 +984,7 @@ static hj_status get_graph(hj_plan* P, int G, cudaGraphExec_t* out) {
 }
 
 hj_status plan_run(hj_plan* P, long long ncycles, float* kernel_ms) {
+  NvtxRange nv("hj_plan_run");
   if (ncycles < 0) { set_error("ncycles must be >= 0"); return HJ_ERR_INVALID_ARG; }
   if (P->peer && !peer_attached(P)) { set_error("peer plan used before hj_plan_peer_attach"); return HJ_ERR_PEER; }
   if (kernel_ms) {
@@ -968,6 +997,7 @@ hj_status plan_run(hj_plan* P, long long ncycles, float* kernel_ms) {
       if (P->evused == 4096) HJ_TRY(drain_events(P, kernel_ms));
     }
     HJ_TRY(drain_events(P, kernel_ms));
+    if (P->dist) HJ_TRY(dist_check(P));
     return HJ_OK;
   }
   long long left = ncycles;
@@ -1045,6 +1075,7 @@ static hj_status run_resident(hj_plan* P, bool* used) {
 }
 
 hj_status plan_solve(hj_plan* P, hj_result* res, double* x_dev, double* hist_dev) {
+  NvtxRange nv("hj_plan_solve");
   const Geom& g = P->g;
   if (P->peer && !peer_attached(P)) { set_error("peer plan used before hj_plan_peer_attach"); return HJ_ERR_PEER; }
   cudaStream_t st = P->stream;
@@ -1068,6 +1099,7 @@ hj_status plan_solve(hj_plan* P, hj_result* res, double* x_dev, double* hist_dev
       P->c_host += G;
       HJ_CUDA(cudaMemcpyAsync(P->ctrl_h, P->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
       HJ_CUDA(cudaStreamSynchronize(st));
+      if (P->dist) HJ_TRY(dist_check(P));
       if (P->ctrl_h->done) break;
       if (G < 256) G *= 2;
     }

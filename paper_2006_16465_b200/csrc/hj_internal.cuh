@@ -123,6 +123,10 @@ struct CycleArgs {
   void* peer_hi = nullptr;
   // multigrid (c24): the snapshot is identically zero (a coarse level's first cycle) — x is not read
   bool zero_x = false;
+  // REG2D only, plans without ragged edge tiles: run only the tile rows ty0 + j * tys, j < nty_run
+  // (nty_run < 0: every tile row).  The overlapped NCCL transport launches the slab's two boundary
+  // tile rows first, sends their rows while the interior tile rows run.
+  int ty0 = 0, tys = 1, nty_run = -1;
 };
 
 // Launchers (kernels_2d.cu / kernels_1d.cu).  Return cudaGetLastError().

@@ -106,6 +106,10 @@ hj_status dist_create(hj_plan* P, const DistInfo* di);
 hj_status dist_initial_exchange(hj_plan* P);
 hj_status dist_halo_exchange(hj_plan* P, int buf);
 hj_status dist_allreduce(hj_plan* P);
+bool dist_overlap(const hj_plan* P);
+hj_status dist_halo_fork(hj_plan* P, int buf);
+hj_status dist_halo_join(hj_plan* P);
+hj_status dist_check(hj_plan* P);
 void dist_free(hj_plan* P);
 
 // peer.cu

@@ -364,7 +364,7 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
              const __grid_constant__ CUtensorMap tmO, T* __restrict__ xout, long long pitch,
              Axis ax, Axis ay, int ntx_full, long long nfull, int ntx, double* __restrict__ part,
              const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt,
-             const __grid_constant__ CUtensorMap tmE, T* peer_lo, T* peer_hi) {
+             const __grid_constant__ CUtensorMap tmE, T* peer_lo, T* peer_hi, int ty0, int tys) {
   if (ctrl->done) return;
   constexpr bool COR = XM == 1, ZX = XM == 2;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
@@ -383,7 +383,7 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
   const long long nw = (long long)gridDim.x * C::WARPS;
   if (gw >= nfull) return;
   auto issue = [&](long long u) {  // u: full-block index; box origin = block's interior origin
-    const int cx = axis_start(ax, (int)(u % ntx_full)), cy = axis_start(ay, (int)(u / ntx_full));
+    const int cx = axis_start(ax, (int)(u % ntx_full)), cy = axis_start(ay, ty0 + (int)(u / ntx_full) * tys);
     mbar_arrive_expect_tx(bar, (ZX ? 0 : C::XBYTES) + C::FBYTES + (COR ? C::EBYTES : 0));
     if (!ZX) tma_load_2d(slot, &tmX, cx, cy, bar);    // x box: padded rows 32ty.., cols 32tx..
     tma_load_2d(slot + C::XSLOT, &tmF, cx, cy, bar);   // h2f box
@@ -402,7 +402,7 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
   int it = 0;
   for (long long u = gw; u < nfull; u += nw, ++it) {
     mbar_wait(bar, it & 1);
-    const int tx = (int)(u % ntx_full), ty = (int)(u / ntx_full);
+    const int tx = (int)(u % ntx_full), ty = ty0 + (int)(u / ntx_full) * tys;
     const int x0 = axis_start(ax, tx), y0 = axis_start(ay, ty);
     reg2d_tile<T, C, MASK, SK, XM>(
         wt, sx, sf, so, hb, lane, kk, part, (long long)ty * ntx + tx,
@@ -781,7 +781,10 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
     // o > 0: every block is a full 32x32 tile (the last one shifted), owned-point stores.
     const bool ovl = g.ox || g.oy;
     const long long ntx_full = ovl ? g.ntx : g.nx / 32, nty_full = ovl ? g.nty : g.ny / 32;
-    const long long nfull = ntx_full * nty_full;
+    const bool subset = a.nty_run >= 0;  // a subset of the tile rows (no edge tiles, checked below)
+    if (subset && (ovl || g.nx % 32 || g.ny % 32 || a.ty0 + (long long)(a.nty_run - 1) * a.tys >= nty_full))
+      return cudaErrorInvalidValue;
+    const long long nfull = ntx_full * (subset ? a.nty_run : nty_full);
     if (nfull > 0) {
       auto go = [&](auto cfg, auto mask, auto cor) {
         using C = decltype(cfg);
@@ -791,7 +794,7 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
             <<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
                 *a.tm_in, *a.tm_f, *a.tm_out, (T*)a.xout, g.pitch, g.ax, g.ay, (int)ntx_full, nfull,
                 (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles, wt, a.tm_cor ? *a.tm_cor : *a.tm_in,
-                (T*)a.peer_lo, (T*)a.peer_hi);
+                (T*)a.peer_lo, (T*)a.peer_hi, subset ? a.ty0 : 0, subset ? a.tys : 1);
       };
       using X0 = std::integral_constant<int, 0>;
       using X1 = std::integral_constant<int, 1>;
@@ -813,7 +816,7 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
         go(R2<T>{}, std::false_type{}, X0{});
       }
     }
-    const long long nedge = g.ntiles - nfull;
+    const long long nedge = subset ? 0 : g.ntiles - nfull;
     if (nedge > 0)
       smem2d_kernel<T, SK><<<(unsigned)nedge, dim3(32, 32), smem_paper, st>>>(
           (const T*)a.xin, (T*)a.xout, (const T*)a.h2f, g.pitch, g.fpitch, (int)g.nx, (int)g.ny,
