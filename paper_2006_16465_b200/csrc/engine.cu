@@ -911,15 +911,21 @@ hj_status launch_cycle(hj_plan* P, int p, bool timed, float* acc_ms) {
     HJ_CUDA(cudaEventRecord(e0, st));
   }
   const bool ovl = dist_overlap(P);
+  // HJ_SPLIT_CYCLE=1 (tests): the overlapped transport's split launch order (boundary tile rows,
+  // then interior tile rows) on any REG2D plan without edge tiles, so its kernel path is exercised
+  // where NCCL cannot run with several ranks (one GPU)
+  static const bool split_env = [] { const char* e = std::getenv("HJ_SPLIT_CYCLE"); return e && e[0] == '1'; }();
+  const bool split = ovl || (split_env && g.dim == 2 && g.kernel_kind == K_REG2D && !g.ox && !g.oy &&
+                             g.nx % 32 == 0 && g.ny % 32 == 0 && g.ny / 32 >= 3 && !a.cor_e && !a.zero_x);
   cudaError_t e;
-  if (ovl) {
+  if (split) {
     // overlapped NCCL transport: the slab's boundary tile rows first, their rows sent
     // on the comm stream while the interior tile rows run, joined before the next cycle
     const int nty = (int)(g.ny / 32);
     a.ty0 = 0; a.tys = nty - 1; a.nty_run = 2;
     e = launch_cycle_2d(g, a, P->nsm, st);
     if (e == cudaSuccess) {
-      HJ_TRY(dist_halo_fork(P, p ^ 1));
+      if (ovl) HJ_TRY(dist_halo_fork(P, p ^ 1));
       a.ty0 = 1; a.tys = 1; a.nty_run = nty - 2;
       e = launch_cycle_2d(g, a, P->nsm, st);
     }

@@ -223,6 +223,204 @@ struct TileD {
   }
 };
 
+// ---- A2: A with a conflict-free halo layout (one 8-B load per use, 8 / 16 distinct words per load) ----
+//   hb[0..63]:  W/E halo, word (i * 8 + 2 * ly + isE)   (row i = 8 ly + i of the tile)
+//   hb[64..127]: S/N halo, word (c * 16 + 2 * lx + isN)  (column 4 lx + c)
+struct TileA2 : TileA {
+  const double* hx2;  // hb + 2 * ly + (lx == 7)       (lx == 0 reads W, others E: only lx 0 / 7 use it)
+  const double* hy2;  // hb + 64 + 2 * lx + (ly == 3)
+  __device__ __forceinline__ void exchange_ns2(int ly, double (&up)[4], double (&dn)[4]) const {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      up[c] = __shfl_down_sync(FULL, x[0][c], 8);
+      dn[c] = __shfl_up_sync(FULL, x[7][c], 8);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double hv = hy2[16 * c];
+      up[c] = ly == 3 ? hv : up[c];
+      dn[c] = ly == 0 ? hv : dn[c];
+    }
+  }
+  __device__ __forceinline__ void sweep2(int lx, int ly) {
+    double up[4], dn[4];
+    exchange_ns2(ly, up, dn);
+    double olo[4], ohi[4];
+#pragma unroll
+    for (int step = 0; step < 8; ++step) {
+      const int i = step == 0 ? 3 : (step & 1) ? 3 + (step + 1) / 2 : 3 - step / 2;
+      const bool hi_side = step > 0 && (step & 1);
+      double w = __shfl_up_sync(FULL, x[i][3], 1, 8);
+      double e = __shfl_down_sync(FULL, x[i][0], 1, 8);
+      const double hv = hx2[8 * i];
+      w = lx == 0 ? hv : w;
+      e = lx == 7 ? hv : e;
+      double nw[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double W = c == 0 ? w : x[i][c - 1];
+        const double E = c == 3 ? e : x[i][c + 1];
+        const double S = (i == 0) ? dn[c] : (step > 0 && hi_side ? ohi[c] : x[i - 1][c]);
+        const double N = (i == 7) ? up[c] : (step > 0 && !hi_side ? olo[c] : x[i + 1][c]);
+        nw[c] = upd2(W, E, S, N, q[i][c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (step == 0) { olo[c] = x[i][c]; ohi[c] = x[i][c]; }
+        else if (hi_side) ohi[c] = x[i][c];
+        else olo[c] = x[i][c];
+        x[i][c] = nw[c];
+      }
+    }
+  }
+};
+
+// ---- experiments: A with parts removed (WRONG results; they only locate the cost) ----
+//   F = 1: no halo selects (edge lanes use the shuffled value);  F = 2: no W/E shuffles (own values);
+//   F = 3: neither;  F = 4: no N/S shuffles
+template <int F>
+struct TileX : TileA {
+  __device__ __forceinline__ void sweepx(int lx, int ly) {
+    double up[4], dn[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      up[c] = F == 4 ? x[0][c] : __shfl_down_sync(FULL, x[0][c], 8);
+      dn[c] = F == 4 ? x[7][c] : __shfl_up_sync(FULL, x[7][c], 8);
+    }
+    if (F != 1 && F != 3) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double hv = hyp[c];
+        up[c] = ly == 3 ? hv : up[c];
+        dn[c] = ly == 0 ? hv : dn[c];
+      }
+    }
+    double olo[4], ohi[4];
+#pragma unroll
+    for (int step = 0; step < 8; ++step) {
+      const int i = step == 0 ? 3 : (step & 1) ? 3 + (step + 1) / 2 : 3 - step / 2;
+      const bool hi_side = step > 0 && (step & 1);
+      double w = (F == 2 || F == 3) ? x[i][3] : __shfl_up_sync(FULL, x[i][3], 1, 8);
+      double e = (F == 2 || F == 3) ? x[i][0] : __shfl_down_sync(FULL, x[i][0], 1, 8);
+      if (F != 1 && F != 3) {
+        const double hv = hxp[i];
+        w = lx == 0 ? hv : w;
+        e = lx == 7 ? hv : e;
+      }
+      double nw[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double W = c == 0 ? w : x[i][c - 1];
+        const double E = c == 3 ? e : x[i][c + 1];
+        const double S = (i == 0) ? dn[c] : (step > 0 && hi_side ? ohi[c] : x[i - 1][c]);
+        const double N = (i == 7) ? up[c] : (step > 0 && !hi_side ? olo[c] : x[i + 1][c]);
+        nw[c] = upd2(W, E, S, N, q[i][c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (step == 0) { olo[c] = x[i][c]; ohi[c] = x[i][c]; }
+        else if (hi_side) ohi[c] = x[i][c];
+        else olo[c] = x[i][c];
+        x[i][c] = nw[c];
+      }
+    }
+  }
+  __device__ __forceinline__ void sweep(int lx, int ly) { sweepx(lx, ly); }
+};
+
+// ---- P: A with the frozen halo written by PREDICATED shared loads into the shuffled registers
+// (edge lanes only; no selects): 1 instruction per halo value instead of 1 load + 2 FSEL ----
+__device__ __forceinline__ void ld_if(double& v, const double* p, bool pred) {
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.f64 %0, [%1];\n}\n"
+               : "+d"(v)
+               : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"((int)pred));
+}
+struct TileP : TileA {
+  __device__ __forceinline__ void sweep(int lx, int ly) {
+    double up[4], dn[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      up[c] = __shfl_down_sync(FULL, x[0][c], 8);
+      dn[c] = __shfl_up_sync(FULL, x[7][c], 8);
+      ld_if(up[c], hyp + c, ly == 3);
+      ld_if(dn[c], hyp + c, ly == 0);
+    }
+    double olo[4], ohi[4];
+#pragma unroll
+    for (int step = 0; step < 8; ++step) {
+      const int i = step == 0 ? 3 : (step & 1) ? 3 + (step + 1) / 2 : 3 - step / 2;
+      const bool hi_side = step > 0 && (step & 1);
+      double w = __shfl_up_sync(FULL, x[i][3], 1, 8);
+      double e = __shfl_down_sync(FULL, x[i][0], 1, 8);
+      ld_if(w, hxp + i, lx == 0);
+      ld_if(e, hxp + i, lx == 7);
+      double nw[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double W = c == 0 ? w : x[i][c - 1];
+        const double E = c == 3 ? e : x[i][c + 1];
+        const double S = (i == 0) ? dn[c] : (step > 0 && hi_side ? ohi[c] : x[i - 1][c]);
+        const double N = (i == 7) ? up[c] : (step > 0 && !hi_side ? olo[c] : x[i + 1][c]);
+        nw[c] = upd2(W, E, S, N, q[i][c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (step == 0) { olo[c] = x[i][c]; ohi[c] = x[i][c]; }
+        else if (hi_side) ohi[c] = x[i][c];
+        else olo[c] = x[i][c];
+        x[i][c] = nw[c];
+      }
+    }
+  }
+};
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+bench_a2(const double* __restrict__ X, const double* __restrict__ Q, double* __restrict__ out, int tiles_per_warp,
+         int k, long long* clk) {
+  __shared__ __align__(16) double hb_all[WARPS][128];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lx = lane & 7, ly = lane >> 3;
+  double* hb = hb_all[warp];
+  const long long gw = (long long)blockIdx.x * WARPS + warp;
+  long long t0 = clock64();
+  double acc = 0.0;
+  for (int t = 0; t < tiles_per_warp; ++t) {
+    const long long src = ((gw * 7 + t) & 255) * 2048;
+    TileA2 tl;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        tl.x[i][c] = __ldcg(X + src + (8 * ly + i) * 32 + 4 * lx + c);
+        tl.q[i][c] = __ldcg(Q + src + (8 * ly + i) * 32 + 4 * lx + c);
+      }
+    // lane = tile row r (W, E) / tile column r (S, N)
+    {
+      const int r = lane, rly = r >> 3, ri = r & 7;
+      hb[ri * 8 + 2 * rly + 0] = __ldcg(X + src + 1024 + r);        // W of row r
+      hb[ri * 8 + 2 * rly + 1] = __ldcg(X + src + 1024 + 32 + r);   // E of row r
+      const int rlx = r >> 2, rc = r & 3;
+      hb[64 + rc * 16 + 2 * rlx + 0] = __ldcg(X + src + 1024 + 64 + r);  // S of column r
+      hb[64 + rc * 16 + 2 * rlx + 1] = __ldcg(X + src + 1024 + 96 + r);  // N of column r
+    }
+    __syncwarp();
+    tl.hx2 = hb + 2 * ly + (lx == 7 ? 1 : 0);
+    tl.hy2 = hb + 64 + 2 * lx + (ly == 3 ? 1 : 0);
+#pragma unroll 1
+    for (int s = 0; s < k; s += 2) {
+      tl.sweep2(lx, ly);
+      tl.sweep2(lx, ly);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc += tl.x[i][c];
+    __syncwarp();
+  }
+  out[gw * 32 + lane] = acc;
+  if (threadIdx.x == 0 && blockIdx.x == 0) *clk = clock64() - t0;
+}
+
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 bench_c(const double* __restrict__ X, const double* __restrict__ Q, double* __restrict__ out, int tiles_per_warp,
@@ -441,6 +639,13 @@ int main(int argc, char** argv) {
   cudaMemcpy(Q, h, n * 8, cudaMemcpyHostToDevice);
   printf("k = %d sub-iterations per tile\n", k);
   run<TileA, 8, 1>("A middle-out (r1)", X, Q, out, clk, nsm, k);
+  run_k("A2 conflict-free halo", bench_a2<8>, 8, 0, X, Q, out, clk, nsm, k);
+  run<TileP, 8, 1>("P predicated halo loads", X, Q, out, clk, nsm, k);
+  run<TileX<1>, 8, 1>("X1 no halo selects", X, Q, out, clk, nsm, k);
+  run<TileX<2>, 8, 1>("X2 no W/E shuffles", X, Q, out, clk, nsm, k);
+  run<TileX<3>, 8, 1>("X3 no W/E shfl, no sel", X, Q, out, clk, nsm, k);
+  run<TileX<4>, 8, 1>("X4 no N/S shuffles", X, Q, out, clk, nsm, k);
+  if (argc > 2) return 0;
   run<TileB, 8, 1>("B sequential", X, Q, out, clk, nsm, k);
   run<TileB, 12, 1>("B sequential 12w", X, Q, out, clk, nsm, k);
   run<TileA, 12, 1>("A middle-out 12w", X, Q, out, clk, nsm, k);

@@ -4,6 +4,8 @@ Bar: iterates bitwise equal to the oracle after a fixed number o
 f32 — both sides evaluate the same canonical expression); residual history within 1e-12
 relative (different summation order); cycle counts to tolerance exactly equal.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -11,6 +13,8 @@ import oracle
 from paper_2006_16465_b200 import hj
 from paper_2006_16465_b200.inputs import make_problem
 from tests import _exact
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -357,3 +361,35 @@ def test_paper_1d_workload_counts(k, o, cycles):
     g = hj.jacobi_solve(1, 1024, 1024, p["h"], p["f"], p["bc"], p["x0"], tol=1e-4, max_cycles=10**6,
                         history=False, **kw)
     assert g["converged"] and g["cycles"] == cycles
+
+
+def test_split_cycle_launch_order_bitwise():
+    """The overlapped NCCL transport's launch order — the slab's boundary tile rows first, then the
+    interior tile rows — forced on one GPU with HJ_SPLIT_CYCLE=1 (NCCL cannot run
+    several ranks on one device): iterates bitwise and history 1e-12 against the oracle, the
+    per-cycle path (HJ_RESIDENT=0) through plan graphs, several cycles."""
+    import subprocess
+    import sys
+    import textwrap
+    code = textwrap.dedent("""
+        import numpy as np, oracle
+        from paper_2006_16465_b200 import hj
+        from paper_2006_16465_b200.inputs import make_problem
+        for (nx, ny, k, c) in ((96, 96, 5, 7), (128, 160, 16, 4)):
+            p = make_problem("R", 2, nx, ny)
+            kw = dict(mode="hier", tile=(32, 32), k=k, tol=0.0, max_cycles=c)
+            o = oracle.solve(2, nx, ny, p["h"], p["f"], p["bc"], p["x0"], **kw)
+            g = hj.jacobi_solve(2, nx, ny, p["h"], p["f"], p["bc"], p["x0"], **kw)
+            assert np.array_equal(g["x"], o["x"]), (nx, ny)
+            np.testing.assert_allclose(g["history"], o["history"], rtol=1e-12, atol=0)
+        p = make_problem("P", 2, 96, 96)
+        kw = dict(mode="hier", tile=(32, 32), k=8, tol=1e-6, max_cycles=10**6, history=False)
+        o = oracle.solve(2, 96, 96, p["h"], p["f"], p["bc"], p["x0"], **kw)
+        g = hj.jacobi_solve(2, 96, 96, p["h"], p["f"], p["bc"], p["x0"], **kw)
+        assert g["cycles"] == o["cycles"]
+        print("ok")
+    """)
+    env = dict(os.environ, HJ_SPLIT_CYCLE="1", HJ_RESIDENT="0")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
