@@ -189,6 +189,11 @@ hj_status hj_plan_solve(hj_plan *plan, hj_result *result);
  * environment variable HJ_HIST_CAP lowers the 2^24 limit, for tests).  The history buffer of
  * hj_plan_solve must hold this many doubles; 0 for params == NULL. */
 int64_t hj_history_capacity(const hj_params *params);
+/* The cycle kernel family the plan runs (for tests and benchmark records): 0 = REG2D (32x32 tiles in
+ * registers, TMA-staged), 1 = SMEM2D (the paper's shared-memory design, any tile), 2 = CLASSIC2D,
+ * 3 = REG1D, 4 = SMEM1D, 5 = CLASSIC1D, 6 = REGT (register tiles of shapes 16x16, 32x16, 16x32,
+ * 64x32, 32x64, 64x64, 128x32); -1 for plan == NULL. */
+int32_t hj_plan_kernel_kind(const hj_plan *plan);
 /* Number of launches of library kernels per cycle (for launch accounting). */
 int32_t hj_plan_launches_per_cycle(const hj_plan *plan);
 hj_status hj_plan_destroy(hj_plan *plan);

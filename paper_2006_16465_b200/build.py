@@ -12,8 +12,8 @@ import concurrent.futures as cf
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhj.so")
-SOURCES = ["engine.cu", "kernels_2d.cu", "kernels_1d.cu", "dist.cu", "peer.cu", "mg.cu"]
-HEADERS = ["hj_internal.cuh", "hj_plan.h", os.path.join("..", "..", "include", "hj.h")]
+SOURCES = ["engine.cu", "kernels_2d.cu", "kernels_2dt.cu", "kernels_1d.cu", "dist.cu", "peer.cu", "mg.cu"]
+HEADERS = ["hj_internal.cuh", "hj_plan.h", "reg_tile.cuh", os.path.join("..", "..", "include", "hj.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",

@@ -284,6 +284,7 @@ hj_status ensure_configured(int* nsm) {
       if (r == cudaSuccess) sms[dev] = prop.multiProcessorCount;
       if (r == cudaSuccess) r = configure_2d();
       if (r == cudaSuccess) r = configure_1d();
+      if (r == cudaSuccess) r = configure_2dt();
       err[dev] = r;
       done[dev] = true;
     }
@@ -374,6 +375,13 @@ static hj_status choose_kernel(const hj_problem* pb, const hj_params* pr, int* k
     const bool full = (ox == 0 && oy == 0) || ((ox > 0 || pb->nx % 32 == 0) && (oy > 0 || pb->ny % 32 == 0));
     if (pr->kernel == HJ_KERNEL_AUTO && pr->tile_x == 32 && pr->tile_y == 32 && aligned && full) {
       *kind = K_REG2D;
+      return HJ_OK;
+    }
+    // other tile shapes in registers (kernels_2dt.cu): Poisson, no overlap, whole 32x32 blocks / tiles
+    const long long bx = std::max(pr->tile_x, 32), by = std::max(pr->tile_y, 32);
+    if (pr->kernel == HJ_KERNEL_AUTO && pr->mode == HJ_HIERARCHICAL && !pb->stencil && ox == 0 && oy == 0 &&
+        regt_shape(pr->tile_x, pr->tile_y) && pb->nx % bx == 0 && pb->ny % by == 0) {
+      *kind = K_REGT;
       return HJ_OK;
     }
     const size_t smem = esz * (2 * size_t(pr->tile_x + 2) * (pr->tile_y + 2) + size_t(pr->tile_x) * pr->tile_y);
@@ -514,8 +522,9 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
     set_error("overlapping subdomains are not supported with row slabs");
     return HJ_ERR_INVALID_CONFIG;
   }
+  if (g.kernel_kind == K_REGT && g.ny % std::max(g.ty, 32) != 0) g.kernel_kind = K_SMEM2D;  // slab rows
   switch (g.kernel_kind) {
-    case K_REG2D: case K_SMEM2D:
+    case K_REG2D: case K_SMEM2D: case K_REGT:
       g.ax = make_axis((int)g.nx, g.tx, g.ox);
       g.ay = make_axis((int)g.ny, g.ty, g.oy);
       g.ntx = g.ax.nb;
@@ -538,7 +547,9 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
       g.ntx = (g.nx + CLASSIC1D_CELLS - 1) / CLASSIC1D_CELLS; g.nty = g.ny; g.nrg_global = g.ny; g.rg_offset = 0;
   }
   g.ntiles = g.ntx * g.nty;
-  g.parts_per_row = g.kernel_kind == K_CLASSIC2D ? 4 * g.ntx : g.ntx;
+  g.parts_per_row = g.kernel_kind == K_CLASSIC2D ? 4 * g.ntx
+                   : g.kernel_kind == K_REGT    ? g.ntx * regt_warps_per_tile(g.tx, g.ty)
+                                                : g.ntx;
   g.nparts = g.parts_per_row * g.nty;
   g.nrg_local = g.nty;
   // buffer geometry
@@ -675,7 +686,7 @@ hj_status plan_build(const hj_problem* pb, const hj_params* pr, cudaStream_t st,
       init_q_kernel<float><<<blocks, 256, 0, st>>>((float*)P->H2F, g.fpitch, g.frows, g.nx, g.ny, pb->f, g.h2, (float)scale);
     PCK(cudaGetLastError());
   }
-  if (g.kernel_kind == K_REG2D) {
+  if (g.kernel_kind == K_REG2D || g.kernel_kind == K_REGT) {
     using u64 = uint64_t;
     const uint32_t bw = (uint32_t)((((g.col0 + 33) * esz + 15) / 16) * 16 / esz);
     for (int b = 0; b < 2; ++b) {
@@ -1224,6 +1235,7 @@ hj_status hj_plan_solve(hj_plan* P, hj_result* res) {
 }
 int64_t hj_history_capacity(const hj_params* pr) { return pr ? history_capacity(pr->max_cycles) : 0; }
 int32_t hj_plan_launches_per_cycle(const hj_plan* P) { return P ? launches_per_cycle(P) : 0; }
+int32_t hj_plan_kernel_kind(const hj_plan* P) { return P ? P->g.kernel_kind : -1; }
 hj_status hj_plan_destroy(hj_plan* P) {
   plan_free(P);
   return HJ_OK;

@@ -94,7 +94,8 @@ struct Geom {
   double omega = 1.0;          // damped sub-iterations (multigrid smoother, reading c24); 1 = the paper's
 };
 
-enum KernelKind { K_REG2D = 0, K_SMEM2D = 1, K_CLASSIC2D = 2, K_REG1D = 3, K_SMEM1D = 4, K_CLASSIC1D = 5 };
+enum KernelKind { K_REG2D = 0, K_SMEM2D = 1, K_CLASSIC2D = 2, K_REG1D = 3, K_SMEM1D = 4, K_CLASSIC1D = 5,
+                  K_REGT = 6 /* register tiles of other shapes, kernels_2dt.cu */ };
 
 // Kernel launch descriptor passed to the per-dimension launchers.
 struct CycleArgs {
@@ -132,6 +133,12 @@ struct CycleArgs {
 // Launchers (kernels_2d.cu / kernels_1d.cu).  Return cudaGetLastError().
 cudaError_t launch_cycle_2d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st);
 cudaError_t launch_cycle_1d(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st);
+// REGT (kernels_2dt.cu): tile shapes 16x16, 32x16, 16x32, 64x32, 32x64, 64x64, 128x32 (Poisson, o = 0,
+// no ragged tiles); warps per tile = (tx/32)(ty/32) for tiles of 32 and more, else 1.
+bool regt_shape(int tx, int ty);
+int regt_warps_per_tile(int tx, int ty);
+cudaError_t launch_regt(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st);
+cudaError_t configure_2dt();
 // Resident solves (whole solve in one cooperative launch; kernels_2d.cu / kernels_1d.cu): the tiles'
 // iterates stay in registers across cycles, only halos and residual partials cross the grid.
 // part: 2 x ntiles doubles; bar: 2 zeroed unsigned ints.

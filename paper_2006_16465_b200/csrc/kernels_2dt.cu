@@ -1,0 +1,286 @@
+// 2D hierarchical cycle for tile shapes other than 32x32 (BASELINE config 5's tile sweep):
+// REGT — the register design of kernels_2d.cu (REG2D) generalised.  PAPER.md:380-387 (§4.1): every
+// Tx x Ty subdomain with its one-cell halo is copied on chip, k Jacobi sub-iterations run with the
+// halo frozen, the interior is written back; the tile shape is the method's parameter
+// (PAPER.md:382, the shared-memory formula :389; 32x32 there only because of Volta's 48 KB, :425).
+//
+// The unit of on-chip storage stays a 32x32 BLOCK per warp (lane = 8 rows x 4 columns in
+// registers, TMA-staged like REG2D):
+//  * small tiles (Tx, Ty <= 32; 16x16, 32x16, 16x32): one block holds (32/Tx) x (32/Ty) method
+//    tiles; lanes on a tile edge inside the block take the tile's frozen halo (snapshot values of
+//    the neighbouring tile, from the TMA box) instead of the neighbouring lane's value — the same
+//    selects as REG2D, so the same instruction count per update; the residual partial of each tile
+//    is a segmented warp reduction.
+//  * large tiles (Tx, Ty >= 32; 64x32, 32x64, 64x64, 128x32): one tile = a group of
+//    (Tx/32) x (Ty/32) warps of one CTA, each holding one block; after every sub-iteration the
+//    warps of a tile write their block-edge rows / columns into the neighbouring warps' halo
+//    buffers (double-buffered by sub-iteration parity) and meet at a named barrier; tile edges keep
+//    the frozen halo.  The iterate is exactly the method's: every cell sees the previous
+//    sub-iteration's values of its in-tile neighbours and the frozen snapshot outside the tile.
+// Poisson, o = 0, nx and ny multiples of max(Tx, 32) / max(Ty, 32) (engine.cu choose_kernel);
+// everything else runs on smem2d_kernel.
+#include "hj_internal.cuh"
+#include "reg_tile.cuh"
+
+namespace hj {
+
+namespace {
+
+using namespace rt;
+
+template <typename T, int TX, int TY>
+struct RT {
+  using C = R2<T>;  // slot layout (x box with halo, q box) shared with REG2D
+  static constexpr bool BIG = TX >= 32 && TY >= 32;
+  static_assert(BIG || (TX <= 32 && TY <= 32 && TX >= 8 && TY >= 16), "tile shape");
+  static constexpr int SBX = BIG ? TX / 32 : 1, SBY = BIG ? TY / 32 : 1;   // blocks per tile
+  static constexpr int WPT = SBX * SBY;                                    // warps per tile
+  static constexpr int TXL = BIG ? 8 : TX / 4, TYL = BIG ? 4 : TY / 8;     // lanes per tile in a block
+  static constexpr int TPX = BIG ? 1 : 32 / TX, TPY = BIG ? 1 : 32 / TY;   // tiles per block
+  // halo buffer (per parity): HX = 8 lane-columns x 32 rows (the W or E column each lane-column
+  // reads), HY = 4 lane-rows x 32 columns (the S or N row each lane-row reads)
+  static constexpr int HX = 8 * 32, HY = 4 * 32;
+  static constexpr int NPAR = WPT > 1 ? 2 : 1;
+  static constexpr int HBYTES = ((HX + HY) * (int)sizeof(T) * NPAR + 127) / 128 * 128;
+  static constexpr int WSMEM = C::XSLOT + C::FBYTES + HBYTES;
+  static constexpr int WARPS = sizeof(T) == 8 ? 8 : (WPT == 1 ? 12 : 8);
+  static_assert(WARPS % WPT == 0, "warps per CTA");
+  static constexpr int GROUPS = WARPS / WPT;
+  static constexpr size_t SMEM = 128 + 128 + size_t(WARPS) * WSMEM;
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+__device__ __forceinline__ void group_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <typename T, int TX, int TY>
+__global__ void __launch_bounds__(RT<T, TX, TY>::WARPS * 32, 1)
+regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
+            T* __restrict__ xout, long long pitch, long long nunits, int units_x, double* __restrict__ part,
+            long long ppr, const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
+  using R = RT<T, TX, TY>;
+  using C = typename R::C;
+  using V2 = typename VecOf<T>::v2;
+  if (ctrl->done) return;
+  const int kk = (ctrl->c >= max_cycles) ? 0 : k;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lx = lane & 7, ly = lane >> 3;
+  const int grp = warp / R::WPT, wg = warp % R::WPT, sbx = wg % R::SBX, sby = wg / R::SBX;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base) + warp;
+  auto slot_of = [&](int w) { return base + 128 + size_t(w) * R::WSMEM; };
+  unsigned char* slot = slot_of(warp);
+  const T* sx = reinterpret_cast<const T*>(slot);
+  const T* sf = reinterpret_cast<const T*>(slot + C::XSLOT);
+  T* hb = reinterpret_cast<T*>(slot + C::XSLOT + C::FBYTES);          // [par][HX + HY]
+  auto halo_of = [&](int w) { return reinterpret_cast<T*>(slot_of(w) + C::XSLOT + C::FBYTES); };
+  const long long gg = (long long)blockIdx.x * R::GROUPS + grp;
+  const long long ng = (long long)gridDim.x * R::GROUPS;
+  if (gg >= nunits) return;  // the whole group leaves together (named barriers stay balanced)
+  // unit u -> this warp's 32x32 block origin (0-based interior coordinates)
+  auto origin = [&](long long u, int& x0, int& y0) {
+    const int ux = (int)(u % units_x), uy = (int)(u / units_x);
+    x0 = R::BIG ? ux * TX + 32 * sbx : 32 * ux;
+    y0 = R::BIG ? uy * TY + 32 * sby : 32 * uy;
+  };
+  auto issue = [&](long long u) {
+    int x0, y0;
+    origin(u, x0, y0);
+    mbar_arrive_expect_tx(bar, C::XBYTES + C::FBYTES);
+    tma_load_2d(slot, &tmX, x0, y0, bar);
+    tma_load_2d(slot + C::XSLOT, &tmF, x0, y0, bar);
+  };
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    prefetch_tensormap(&tmX);
+    prefetch_tensormap(&tmF);
+    issue(gg);
+  }
+  __syncwarp();
+  using TL = Tile2<T, false, 0, R::TXL, R::TYL>;
+  // halo pointers: lane-column lx reads column (W edge ? 4lx-1 : 4lx+4) of its rows, lane-row ly
+  // reads row (S edge ? 8ly-1 : 8ly+8) of its columns (block-local, -1 / 32 = the TMA box's ring)
+  const int hxo = lx * 32 + 8 * ly, hyo = R::HX + ly * 32 + 4 * lx;
+  const int bar_id = 1 + grp, bar_n = 32 * R::WPT;
+  int it = 0;
+  for (long long u = gg; u < nunits; u += ng, ++it) {
+    mbar_wait(bar, it & 1);
+    int x0, y0;
+    origin(u, x0, y0);
+    TL tl;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {  // 128-bit shared loads
+      const int r = 8 * ly + i;
+      const V2* rowx = reinterpret_cast<const V2*>(sx + (r + 1) * C::BW + C::COL0 + 4 * lx);
+      const V2* rowf = reinterpret_cast<const V2*>(sf + r * 32 + 4 * lx);
+      const V2 a = rowx[0], b = rowx[1], fa = rowf[0], fb = rowf[1];
+      tl.x[i][0] = a.x; tl.x[i][1] = a.y; tl.x[i][2] = b.x; tl.x[i][3] = b.y;
+      tl.q[i][0] = fa.x; tl.q[i][1] = fa.y; tl.q[i][2] = fb.x; tl.q[i][3] = fb.y;
+    }
+    // frozen halo of the snapshot, for every lane-column / lane-row (both parities for tile groups:
+    // the block edges inside a tile are overwritten by the neighbours after each sub-iteration)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int col = TL::eW(c) ? 4 * c - 1 : 4 * c + 4;
+      const T v = sx[(lane + 1) * C::BW + C::COL0 + col];
+#pragma unroll
+      for (int p = 0; p < R::NPAR; ++p) hb[p * (R::HX + R::HY) + c * 32 + lane] = v;
+    }
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int row = TL::eS(l) ? 8 * l - 1 : 8 * l + 8;
+      const T v = sx[(row + 1) * C::BW + C::COL0 + lane];
+#pragma unroll
+      for (int p = 0; p < R::NPAR; ++p) hb[p * (R::HX + R::HY) + R::HX + l * 32 + lane] = v;
+    }
+    tl.hxp = hb + hxo;
+    tl.hyp = hb + hyo;
+    tl.own = 0xffffffffu;
+    __syncwarp();
+    if (lane == 0 && u + ng < nunits) {  // the slot is in registers / the halo buffer: refill
+      fence_proxy_async();
+      issue(u + ng);
+    }
+    if constexpr (R::WPT > 1) group_bar(bar_id, bar_n);  // every warp of the tile filled its halo
+    // fused residual of the snapshot folded into the first sub-iteration (f64); separate pass (f32)
+    constexpr bool FOLD = sizeof(T) == 8;
+    double acc = 0.0;
+    if (!FOLD || kk == 0) acc = tl.residual(lx, ly);
+    int s = 0;
+    auto exchange = [&](int s_next) {  // block edges -> the neighbouring warps' buffers (parity s_next)
+      if constexpr (R::WPT > 1) {
+        const int po = (s_next & 1) * (R::HX + R::HY);
+        if (sbx > 0 && lx == 0) {        // my column 0 -> W neighbour's E column (its lane-column 7)
+          T* d = halo_of(warp - 1) + po + 7 * 32 + 8 * ly;
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) *reinterpret_cast<V2*>(d + i) = V2{tl.x[i][0], tl.x[i + 1][0]};
+        }
+        if (sbx < R::SBX - 1 && lx == 7) {  // my column 31 -> E neighbour's W column (lane-column 0)
+          T* d = halo_of(warp + 1) + po + 0 * 32 + 8 * ly;
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) *reinterpret_cast<V2*>(d + i) = V2{tl.x[i][3], tl.x[i + 1][3]};
+        }
+        if (sby > 0 && ly == 0) {        // my row 0 -> S neighbour's N row (its lane-row 3)
+          T* d = halo_of(warp - R::SBX) + po + R::HX + 3 * 32 + 4 * lx;
+          reinterpret_cast<V2*>(d)[0] = V2{tl.x[0][0], tl.x[0][1]};
+          reinterpret_cast<V2*>(d)[1] = V2{tl.x[0][2], tl.x[0][3]};
+        }
+        if (sby < R::SBY - 1 && ly == 3) {  // my row 31 -> N neighbour's S row (lane-row 0)
+          T* d = halo_of(warp + R::SBX) + po + R::HX + 0 * 32 + 4 * lx;
+          reinterpret_cast<V2*>(d)[0] = V2{tl.x[7][0], tl.x[7][1]};
+          reinterpret_cast<V2*>(d)[1] = V2{tl.x[7][2], tl.x[7][3]};
+        }
+        group_bar(bar_id, bar_n);
+        tl.hxp = hb + po + hxo;
+        tl.hyp = hb + po + hyo;
+      }
+    };
+    if (FOLD && kk > 0) {
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};
+      tl.template sweep_mo<true>(lx, ly, a4);
+      acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      s = 1;
+      if (s < kk) exchange(s);
+    }
+#pragma unroll 1
+    for (; s < kk; ++s) {
+      tl.template sweep_mo<false>(lx, ly);
+      if (s + 1 < kk) exchange(s + 1);
+    }
+    // residual partials: per tile (small tiles: segmented reduction over the tile's lanes)
+    if constexpr (R::BIG) {
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        const long long ux = u % units_x, uy = u / units_x;
+        part[uy * ppr + ux * R::WPT + wg] = acc;
+      }
+    } else {
+#pragma unroll
+      for (int o = 1; o < R::TXL; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
+#pragma unroll
+      for (int o = 1; o < R::TYL; o <<= 1) acc += __shfl_xor_sync(FULL, acc, 8 * o);
+      if (lx % R::TXL == 0 && ly % R::TYL == 0) {
+        const long long tx = x0 / TX + lx / R::TXL, ty = y0 / TY + ly / R::TYL;
+        part[ty * ppr + tx] = acc;
+      }
+    }
+    if (kk > 0) {  // registers -> the NEXT iterate, 128-bit stores (snapshot semantics)
+      T* g = xout + ((long long)y0 + 1) * pitch + C::COL0 + x0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        V2* dst = reinterpret_cast<V2*>(g + (8 * ly + i) * pitch + 4 * lx);
+        dst[0] = V2{tl.x[i][0], tl.x[i][1]};
+        dst[1] = V2{tl.x[i][2], tl.x[i][3]};
+      }
+    }
+    // the next tile's halo fill must not overwrite buffers a neighbour still reads
+    if constexpr (R::WPT > 1) group_bar(bar_id, bar_n);
+  }
+}
+
+template <typename T, int TX, int TY>
+cudaError_t launch_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
+  using R = RT<T, TX, TY>;
+  const long long units_x = R::BIG ? g.nx / TX : g.nx / 32;
+  const long long nunits = R::BIG ? units_x * (g.ny / TY) : units_x * (g.ny / 32);
+  long long ctas = (nunits + R::GROUPS - 1) / R::GROUPS;
+  if (ctas > grid_hint) ctas = grid_hint;
+  regt_kernel<T, TX, TY><<<(unsigned)ctas, R::WARPS * 32, R::SMEM, st>>>(
+      *a.tm_in, *a.tm_f, (T*)a.xout, g.pitch, nunits, (int)units_x, a.part, g.parts_per_row, a.ctrl, g.k,
+      a.max_cycles);
+  return cudaGetLastError();
+}
+
+template <typename T, int TX, int TY>
+cudaError_t cfg_t() {
+  return cudaFuncSetAttribute(regt_kernel<T, TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)RT<T, TX, TY>::SMEM);
+}
+
+template <typename T>
+cudaError_t launch_regt_T(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
+  const int tx = g.tx, ty = g.ty;
+  if (tx == 16 && ty == 16) return launch_t<T, 16, 16>(g, a, grid_hint, st);
+  if (tx == 32 && ty == 16) return launch_t<T, 32, 16>(g, a, grid_hint, st);
+  if (tx == 16 && ty == 32) return launch_t<T, 16, 32>(g, a, grid_hint, st);
+  if (tx == 64 && ty == 32) return launch_t<T, 64, 32>(g, a, grid_hint, st);
+  if (tx == 32 && ty == 64) return launch_t<T, 32, 64>(g, a, grid_hint, st);
+  if (tx == 64 && ty == 64) return launch_t<T, 64, 64>(g, a, grid_hint, st);
+  if (tx == 128 && ty == 32) return launch_t<T, 128, 32>(g, a, grid_hint, st);
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+cudaError_t cfg_T() {
+  cudaError_t e;
+  if ((e = cfg_t<T, 16, 16>()) != cudaSuccess) return e;
+  if ((e = cfg_t<T, 32, 16>()) != cudaSuccess) return e;
+  if ((e = cfg_t<T, 16, 32>()) != cudaSuccess) return e;
+  if ((e = cfg_t<T, 64, 32>()) != cudaSuccess) return e;
+  if ((e = cfg_t<T, 32, 64>()) != cudaSuccess) return e;
+  if ((e = cfg_t<T, 64, 64>()) != cudaSuccess) return e;
+  return cfg_t<T, 128, 32>();
+}
+
+}  // namespace
+
+// The tile shapes REGT runs (the rest of engine.cu's choice is in choose_kernel).
+bool regt_shape(int tx, int ty) {
+  return (tx == 16 && ty == 16) || (tx == 32 && ty == 16) || (tx == 16 && ty == 32) || (tx == 64 && ty == 32) ||
+         (tx == 32 && ty == 64) || (tx == 64 && ty == 64) || (tx == 128 && ty == 32);
+}
+int regt_warps_per_tile(int tx, int ty) { return tx >= 32 && ty >= 32 ? (tx / 32) * (ty / 32) : 1; }
+
+cudaError_t launch_regt(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
+  return g.dtype == HJ_F64 ? launch_regt_T<double>(g, a, grid_hint, st) : launch_regt_T<float>(g, a, grid_hint, st);
+}
+
+cudaError_t configure_2dt() {
+  cudaError_t e = cfg_T<double>();
+  return e != cudaSuccess ? e : cfg_T<float>();
+}
+
+}  // namespace hj

@@ -26,6 +26,7 @@ MODES = {"hier": 0, "hierarchical": 0, "classic": 1, "mg": 2, "multigrid": 2}
 DTYPES = {"f64": 0, "float64": 0, "f32": 1, "float32": 1}
 TOL_MODES = {"rel": 0, "relative": 0, "abs": 1, "absolute": 1}
 KERNELS = {"auto": 0, "smem": 1}
+KERNEL_KINDS = {0: "reg2d", 1: "smem2d", 2: "classic2d", 3: "reg1d", 4: "smem1d", 5: "classic1d", 6: "regt"}
 
 _P = ctypes.c_void_p
 
@@ -110,6 +111,8 @@ def lib():
         L.hj_last_error.argtypes = []
         L.hj_history_capacity.restype = ctypes.c_int64
         L.hj_history_capacity.argtypes = [ctypes.POINTER(hj_params)]
+        L.hj_plan_kernel_kind.restype = ctypes.c_int32
+        L.hj_plan_kernel_kind.argtypes = [_P]
         L.hj_plan_launches_per_cycle.restype = ctypes.c_int32
         L.hj_plan_launches_per_cycle.argtypes = [_P]
         _lib = L
@@ -282,6 +285,9 @@ class Plan:
         # the history is truncated at the capacity (include/hj.h)
         return _result(res, st, x.view(self.ny, self.nx) if self.dim == 2 or self.ny > 1 else x,
                        None if hist is None else hist[: min(res.cycles + 1, cap)])
+
+    def kernel_kind(self) -> str:
+        return KERNEL_KINDS.get(lib().hj_plan_kernel_kind(self._p), "?")
 
     def launches_per_cycle(self):
         return lib().hj_plan_launches_per_cycle(self._p)

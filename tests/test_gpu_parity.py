@@ -393,3 +393,41 @@ def test_split_cycle_launch_order_bitwise():
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+REGT_CASES = [  # (nx, ny, tile): BASELINE config 5's tile sweep shapes on small grids (several tiles each way)
+    (96, 64, (16, 16)), (64, 96, (32, 16)), (96, 64, (16, 32)), (192, 96, (64, 32)), (96, 192, (32, 64)),
+    (128, 192, (64, 64)), (256, 96, (128, 32)),
+]
+
+
+@pytest.mark.parametrize("nx,ny,tile", REGT_CASES, ids=[f"{t[0]}x{t[1]}" for _, _, t in REGT_CASES])
+@pytest.mark.parametrize("k", [1, 4, 7])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_regt_tile_shapes_bitwise(nx, ny, tile, k, dtype):
+    """The register kernel for other tile shapes (kernels_2dt.cu; several tiles per warp, or a warp
+    group per tile with a per-sub-iteration block-edge exchange) equals the oracle bit for bit, history
+    1e-12, and the plan really runs it (hj_plan_kernel_kind)."""
+    import torch
+    p = make_problem("R", 2, nx, ny)
+    kw = dict(mode="hier", tile=tile, k=k, dtype=dtype, tol=0.0, max_cycles=3)
+    o = oracle.solve(2, nx, ny, p["h"], p["f"], p["bc"], p["x0"], **kw)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.as_tensor(a, device=dev)
+    plan = hj.Plan(2, nx, ny, p["h"], t(p["f"]), t(p["bc"]), t(p["x0"]), **kw)
+    assert plan.kernel_kind() == "regt"
+    r = plan.solve()
+    plan.close()
+    assert np.array_equal(r["x"].cpu().numpy(), o["x"])
+    np.testing.assert_allclose(r["history"].cpu().numpy(), o["history"], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("tile", [(16, 16), (64, 64), (128, 32)])
+def test_regt_counts_to_tolerance(tile):
+    """Cycle counts to 1e-6 (paper protocol) with the REGT tile shapes equal the oracle's exactly."""
+    n = 128 if tile[0] <= 64 else 256
+    p = make_problem("P", 2, n, 128)
+    kw = dict(mode="hier", tile=tile, k=16, tol=1e-6, max_cycles=10**6, history=False)
+    o = oracle.solve(2, n, 128, p["h"], p["f"], p["bc"], p["x0"], **kw)
+    g = hj.jacobi_solve(2, n, 128, p["h"], p["f"], p["bc"], p["x0"], **kw)
+    assert o["converged"] and g["cycles"] == o["cycles"]
