@@ -46,13 +46,102 @@ struct RT {
   static constexpr int WARPS = sizeof(T) == 8 ? 8 : (WPT == 1 ? 12 : 8);
   static_assert(WARPS % WPT == 0, "warps per CTA");
   static constexpr int GROUPS = WARPS / WPT;
-  static constexpr size_t SMEM = 128 + 128 + size_t(WARPS) * WSMEM;
+  static constexpr int BARS = 512;  // TMA mbarriers [0, 16), halo mbarriers 16 + 4 * warp + 2 * parity + half
+  static constexpr size_t SMEM = 128 + BARS + size_t(WARPS) * WSMEM;
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 __device__ __forceinline__ void group_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+
+// Block-edge exchange of a tile spread over a warp group, one half-sweep at a time (Tile2::sweep_h):
+// after computing rows 3,4,2,5 (half A) of sub-iteration s a warp stores their block-edge values into
+// the W / E neighbours' halo buffers of parity (s+1)&1 and arrives on their half-A mbarrier; after
+// rows 1,6,0,7 (half B) the same for those rows plus its first / last row for the S / N neighbours,
+// arriving on every neighbour's half-B mbarrier.  A warp waits on its own half-A / half-B mbarrier
+// just before the corresponding half of sub-iteration s+1, so neighbours are only ever half a
+// sub-iteration apart — no group-wide barrier per sub-iteration.  Buffer reuse is safe: the
+// parity-p half-A (half-B) buffer is rewritten only after its reader's half-A (half-B) arrival of
+// the sub-iteration that read it.
+__device__ __forceinline__ void sts2(uint32_t a, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
+}
+__device__ __forceinline__ void sts2(uint32_t a, float x, float y) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x), "f"(y) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+// All addresses are 32-bit shared-window addresses derived from the warp index (few live registers):
+//   halo buffer of warp w, parity p:  hb0 + w * WSMEM + p * (HX + HY) * sizeof(T)
+//   halo mbarrier (w, p, half):       mb0 + 8 * (4 w + 2 p + half)
+template <typename T, typename R>
+struct Exch {
+  uint32_t hb0, mb0;      // shared addresses: halo buffer of warp 0, halo mbarrier (0, 0, 0)
+  int warp, lx, ly, lane;
+  int pw;                 // parity written this sub-iteration
+  uint32_t wa, wb, wph;   // my half-A / half-B mbarriers of the parity read, their phase
+  bool do_wait, do_send, hW, hE, hS, hN;
+  __device__ __forceinline__ uint32_t halo(int w) const {
+    return hb0 + (uint32_t)(w * R::WSMEM) + (uint32_t)(pw * (R::HX + R::HY) * (int)sizeof(T));
+  }
+  __device__ __forceinline__ uint32_t mbar(int w, int half) const { return mb0 + 8u * (4 * w + 2 * pw + half); }
+  __device__ __forceinline__ void wait_a() const { if (do_wait && (hW || hE)) mbar_wait_u32(wa, wph); }
+  __device__ __forceinline__ void wait_b() const { if (do_wait) mbar_wait_u32(wb, wph); }
+  template <typename TL>
+  __device__ __forceinline__ void send_a(const TL& t) const {
+    if (!do_send) return;
+    constexpr uint32_t E = sizeof(T);
+    if (hW && lx == 0) {  // my column 0 -> W neighbour's E column (its lane-column 7)
+      const uint32_t q = halo(warp - 1) + (7 * 32 + 8 * ly) * E;
+      sts2(q + 2 * E, t.x[2][0], t.x[3][0]);
+      sts2(q + 4 * E, t.x[4][0], t.x[5][0]);
+    }
+    if (hE && lx == 7) {  // my column 31 -> E neighbour's W column (its lane-column 0)
+      const uint32_t q = halo(warp + 1) + (8 * ly) * E;
+      sts2(q + 2 * E, t.x[2][3], t.x[3][3]);
+      sts2(q + 4 * E, t.x[4][3], t.x[5][3]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (hW) mbar_arrive_u32(mbar(warp - 1, 0));
+      if (hE) mbar_arrive_u32(mbar(warp + 1, 0));
+    }
+  }
+  template <typename TL>
+  __device__ __forceinline__ void send_b(const TL& t) const {
+    if (!do_send) return;
+    constexpr uint32_t E = sizeof(T);
+    if (hW && lx == 0) {
+      const uint32_t q = halo(warp - 1) + (7 * 32 + 8 * ly) * E;
+      sts2(q, t.x[0][0], t.x[1][0]);
+      sts2(q + 6 * E, t.x[6][0], t.x[7][0]);
+    }
+    if (hE && lx == 7) {
+      const uint32_t q = halo(warp + 1) + (8 * ly) * E;
+      sts2(q, t.x[0][3], t.x[1][3]);
+      sts2(q + 6 * E, t.x[6][3], t.x[7][3]);
+    }
+    if (hS && ly == 0) {  // my row 0 -> S neighbour's N row (its lane-row 3)
+      const uint32_t q = halo(warp - R::SBX) + (R::HX + 3 * 32 + 4 * lx) * E;
+      sts2(q, t.x[0][0], t.x[0][1]);
+      sts2(q + 2 * E, t.x[0][2], t.x[0][3]);
+    }
+    if (hN && ly == 3) {  // my row 31 -> N neighbour's S row (its lane-row 0)
+      const uint32_t q = halo(warp + R::SBX) + (R::HX + 4 * lx) * E;
+      sts2(q, t.x[7][0], t.x[7][1]);
+      sts2(q + 2 * E, t.x[7][2], t.x[7][3]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (hW) mbar_arrive_u32(mbar(warp - 1, 1));
+      if (hE) mbar_arrive_u32(mbar(warp + 1, 1));
+      if (hS) mbar_arrive_u32(mbar(warp - R::SBX, 1));
+      if (hN) mbar_arrive_u32(mbar(warp + R::SBX, 1));
+    }
+  }
+};
 
 template <typename T, int TX, int TY>
 __global__ void __launch_bounds__(RT<T, TX, TY>::WARPS * 32, 1)
@@ -70,7 +159,7 @@ regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lx = lane & 7, ly = lane >> 3;
   const int grp = warp / R::WPT, wg = warp % R::WPT, sbx = wg % R::SBX, sby = wg / R::SBX;
   uint64_t* bar = reinterpret_cast<uint64_t*>(base) + warp;
-  auto slot_of = [&](int w) { return base + 128 + size_t(w) * R::WSMEM; };
+  auto slot_of = [&](int w) { return base + R::BARS + size_t(w) * R::WSMEM; };
   unsigned char* slot = slot_of(warp);
   const T* sx = reinterpret_cast<const T*>(slot);
   const T* sf = reinterpret_cast<const T*>(slot + C::XSLOT);
@@ -78,6 +167,20 @@ regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   auto halo_of = [&](int w) { return reinterpret_cast<T*>(slot_of(w) + C::XSLOT + C::FBYTES); };
   const long long gg = (long long)blockIdx.x * R::GROUPS + grp;
   const long long ng = (long long)gridDim.x * R::GROUPS;
+  // internal block edges of my tile (neighbouring warps of the group) and my halo mbarriers
+  const bool hW = sbx > 0, hE = sbx < R::SBX - 1, hS = sby > 0, hN = sby < R::SBY - 1;
+  const int nA = hW + hE, nB = nA + hS + hN;
+  auto hmb = [&](int w, int par, int half) { return reinterpret_cast<uint64_t*>(base) + 16 + 4 * w + 2 * par + half; };
+  if constexpr (R::WPT > 1) {
+    if (lane == 0) {
+      for (int p = 0; p < 2; ++p) {
+        mbar_init(hmb(warp, p, 0), nA > 0 ? nA : 1);
+        mbar_init(hmb(warp, p, 1), nB);
+      }
+      fence_mbar_init();
+    }
+    __syncthreads();  // every halo mbarrier is initialised before any neighbour arrives on it
+  }
   if (gg >= nunits) return;  // the whole group leaves together (named barriers stay balanced)
   // unit u -> this warp's 32x32 block origin (0-based interior coordinates)
   auto origin = [&](long long u, int& x0, int& y0) {
@@ -105,6 +208,7 @@ regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   // reads row (S edge ? 8ly-1 : 8ly+8) of its columns (block-local, -1 / 32 = the TMA box's ring)
   const int hxo = lx * 32 + 8 * ly, hyo = R::HX + ly * 32 + 4 * lx;
   const int bar_id = 1 + grp, bar_n = 32 * R::WPT;
+  uint32_t ph = 0u;  // bit p: phase of my parity-p halo mbarriers
   int it = 0;
   for (long long u = gg; u < nunits; u += ng, ++it) {
     mbar_wait(bar, it & 1);
@@ -149,46 +253,51 @@ regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     constexpr bool FOLD = sizeof(T) == 8;
     double acc = 0.0;
     if (!FOLD || kk == 0) acc = tl.residual(lx, ly);
-    int s = 0;
-    auto exchange = [&](int s_next) {  // block edges -> the neighbouring warps' buffers (parity s_next)
-      if constexpr (R::WPT > 1) {
-        const int po = (s_next & 1) * (R::HX + R::HY);
-        if (sbx > 0 && lx == 0) {        // my column 0 -> W neighbour's E column (its lane-column 7)
-          T* d = halo_of(warp - 1) + po + 7 * 32 + 8 * ly;
-#pragma unroll
-          for (int i = 0; i < 8; i += 2) *reinterpret_cast<V2*>(d + i) = V2{tl.x[i][0], tl.x[i + 1][0]};
+    if constexpr (R::WPT == 1) {
+      int s = 0;
+      if constexpr (FOLD) {
+        if (kk > 0) {
+          double a4[4] = {0.0, 0.0, 0.0, 0.0};
+          tl.template sweep_mo<true>(lx, ly, a4);
+          acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+          s = 1;
         }
-        if (sbx < R::SBX - 1 && lx == 7) {  // my column 31 -> E neighbour's W column (lane-column 0)
-          T* d = halo_of(warp + 1) + po + 0 * 32 + 8 * ly;
-#pragma unroll
-          for (int i = 0; i < 8; i += 2) *reinterpret_cast<V2*>(d + i) = V2{tl.x[i][3], tl.x[i + 1][3]};
-        }
-        if (sby > 0 && ly == 0) {        // my row 0 -> S neighbour's N row (its lane-row 3)
-          T* d = halo_of(warp - R::SBX) + po + R::HX + 3 * 32 + 4 * lx;
-          reinterpret_cast<V2*>(d)[0] = V2{tl.x[0][0], tl.x[0][1]};
-          reinterpret_cast<V2*>(d)[1] = V2{tl.x[0][2], tl.x[0][3]};
-        }
-        if (sby < R::SBY - 1 && ly == 3) {  // my row 31 -> N neighbour's S row (lane-row 0)
-          T* d = halo_of(warp + R::SBX) + po + R::HX + 0 * 32 + 4 * lx;
-          reinterpret_cast<V2*>(d)[0] = V2{tl.x[7][0], tl.x[7][1]};
-          reinterpret_cast<V2*>(d)[1] = V2{tl.x[7][2], tl.x[7][3]};
-        }
-        group_bar(bar_id, bar_n);
-        tl.hxp = hb + po + hxo;
-        tl.hyp = hb + po + hyo;
       }
-    };
-    if (FOLD && kk > 0) {
-      double a4[4] = {0.0, 0.0, 0.0, 0.0};
-      tl.template sweep_mo<true>(lx, ly, a4);
-      acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-      s = 1;
-      if (s < kk) exchange(s);
-    }
 #pragma unroll 1
-    for (; s < kk; ++s) {
-      tl.template sweep_mo<false>(lx, ly);
-      if (s + 1 < kk) exchange(s + 1);
+      for (; s < kk; ++s) tl.template sweep_mo<false>(lx, ly);
+    } else {
+      Exch<T, R> ex;
+      ex.hb0 = smem_u32(halo_of(0));
+      ex.mb0 = smem_u32(hmb(0, 0, 0));
+      ex.warp = warp; ex.lx = lx; ex.ly = ly; ex.lane = lane;
+      ex.hW = hW; ex.hE = hE; ex.hS = hS; ex.hN = hN;
+      auto setup = [&](int s) {  // sub-iteration s reads parity s&1 and writes parity (s+1)&1
+        const int pr = s & 1;
+        ex.pw = pr ^ 1;
+        ex.do_wait = s > 0;
+        ex.do_send = s + 1 < kk;
+        ex.wa = ex.mb0 + 8u * (4 * warp + 2 * pr);
+        ex.wb = ex.wa + 8u;
+        ex.wph = (ph >> pr) & 1u;
+        tl.hxp = hb + pr * (R::HX + R::HY) + hxo;
+        tl.hyp = hb + pr * (R::HX + R::HY) + hyo;
+      };
+      int s = 0;
+      if constexpr (FOLD) {
+        if (kk > 0) {
+          double a4[4] = {0.0, 0.0, 0.0, 0.0};
+          setup(0);
+          tl.template sweep_h<true>(lx, ly, a4, ex);
+          acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+          s = 1;
+        }
+      }
+#pragma unroll 1
+      for (; s < kk; ++s) {
+        setup(s);
+        tl.template sweep_h<false>(lx, ly, nullptr, ex);
+        if (s > 0) ph ^= 1u << (s & 1);  // this parity's mbarriers completed one more phase
+      }
     }
     // residual partials: per tile (small tiles: segmented reduction over the tile's lanes)
     if constexpr (R::BIG) {
@@ -216,8 +325,6 @@ regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         dst[1] = V2{tl.x[i][2], tl.x[i][3]};
       }
     }
-    // the next tile's halo fill must not overwrite buffers a neighbour still reads
-    if constexpr (R::WPT > 1) group_bar(bar_id, bar_n);
   }
 }
 

@@ -128,6 +128,54 @@ struct Tile2 {
     return acc;
   }
 
+  // sweep_mo with exchange hooks for tiles spread over several warps (kernels_2dt.cu): the same
+  // rows in the same middle-out order, split in two halves — rows 3,4,2,5 (A) and 1,6,0,7 (B).
+  // h.wait_a() / h.wait_b() before each half (the neighbours' block edges of the previous
+  // sub-iteration for that half have arrived), h.send_a(*this) / h.send_b(*this) after it (my new
+  // block-edge values of that half to the neighbours); the N/S lane exchange moves to just before
+  // row 0 so that it reads the halo rows only after wait_b.  Same values as sweep_mo.
+  template <bool RES, typename H>
+  __device__ __forceinline__ void sweep_h(int lx, int ly, double* acc, H& h) {
+    T up[4], dn[4];
+    T olo[4], ohi[4];
+    h.wait_a();
+#pragma unroll
+    for (int step = 0; step < 8; ++step) {
+      const int i = step == 0 ? 3 : (step & 1) ? 3 + (step + 1) / 2 : 3 - step / 2;  // 3,4,2,5,1,6,0,7
+      const bool hi_side = step > 0 && (step & 1);
+      if (step == 4) h.wait_b();
+      if (step == 6) exchange_ns(ly, up, dn);   // rows 0 and 7 still hold the old values
+      T w, e;
+      exchange_we(lx, i, w, e);
+      T nw[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const T W = c == 0 ? w : x[i][c - 1];
+        const T E = c == 3 ? e : x[i][c + 1];
+        const T S = (i == 0) ? dn[c] : (step > 0 && hi_side ? ohi[c] : x[i - 1][c]);
+        const T N = (i == 7) ? up[c] : (step > 0 && !hi_side ? olo[c] : x[i + 1][c]);
+        if constexpr (RES) {  // Poisson, T = double (the REGT fold)
+          const double sum = __dadd_rn(__dadd_rn(W, E), __dadd_rn(S, N));
+          nw[c] = __fma_rn(0.25, sum, q[i][c]);
+          const double t = __fma_rn(4.0, x[i][c], -sum);
+          const double r = __fma_rn(4.0, q[i][c], -t);
+          acc[c] = __fma_rn(r, r, acc[c]);
+        } else {
+          nw[c] = upd(W, E, S, N, q[i][c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (step == 0) { olo[c] = x[i][c]; ohi[c] = x[i][c]; }
+        else if (hi_side) ohi[c] = x[i][c];
+        else olo[c] = x[i][c];
+        x[i][c] = nw[c];
+      }
+      if (step == 3) h.send_a(*this);
+    }
+    h.send_b(*this);
+  }
+
   // One Jacobi sub-iteration in middle-out row order 3,4,2,5,1,6,0,7: every row's inputs from the
   // previous sub-iteration were produced >= 3 rows earlier, and the cross-lane N/S values (rows 0
   // and 7 of the neighbouring lane rows) are consumed last, so consecutive sub-iterations overlap
