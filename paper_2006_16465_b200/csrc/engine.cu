@@ -1070,6 +1070,14 @@ static hj_status run_resident(hj_plan* P, bool* used) {
   }
   const int k = g.k;
   cudaError_t e;
+  if (res1w_ok(g) && !(std::getenv("HJ_RES1W") && std::getenv("HJ_RES1W")[0] == '0')) {
+    // one small 1D problem: the whole solve in one warp (res1w_kernel)
+    e = launch_resident_1w(g, P->X[0], P->X[1], P->H2F, P->ctrl, P->hist, P->hist_cap, P->prm.tol,
+                           (int)P->prm.tol_mode, P->prm.ref_residual, P->prm.max_cycles, k, P->stream);
+    HJ_CUDA(e);
+    *used = true;
+    return HJ_OK;
+  }
   if (many) {
     // M <= 16: two CTAs per SM (<= 128 registers), M = 32: one
     int M = 2;

@@ -151,6 +151,10 @@ cudaError_t launch_resident_1d(const Geom& g, void* X0, void* X1, const void* Q,
 cudaError_t launch_resident_1dm(const Geom& g, int M, void* X0, void* X1, const void* Q, double* part, double* R,
                                 Ctrl* ctrl, double* hist, long long hist_cap, double tol, int tol_mode,
                                 double ref_residual, long long max_cycles, int k, unsigned int* bar, cudaStream_t st);
+bool res1w_ok(const Geom& g);
+cudaError_t launch_resident_1w(const Geom& g, void* X0, void* X1, const void* Q, Ctrl* ctrl, double* hist,
+                               long long hist_cap, double tol, int tol_mode, double ref_residual,
+                               long long max_cycles, int k, cudaStream_t st);
 size_t reg1d_smem_bytes(int dtype, int tile);
 int reg1d_warps_per_cta(int dtype, int tile);
 cudaError_t reg_kernels_configure();  // opt in to large dynamic shared memory

@@ -341,6 +341,114 @@ res1d_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, lo
 }
 
 // =============================================================================
+// RES1W — the resident solver for ONE small 1D problem (nx = 32 C <= 1024 points, e.g. BASELINE config
+// 1: N = 256, 8 tiles of 32, k = 16, tol 1e-8): the whole problem in ONE warp, C consecutive points
+// per lane, every tile a run of tx / C lanes.  No CTA barrier, no shared memory, no per-cycle global
+// traffic: per cycle the tile-edge lanes take the frozen halo of x_c by one shuffle each way, the k
+// sub-iterations run in registers (the first with the residual of x_c folded in, fp64), one warp
+// reduction and every lane takes the same stopping decision (hj_decide on the broadcast sum).  The
+// iterate x_c is kept beside x_{c+1} so that a converged solve returns the snapshot it tested.
+// Same per-point arithmetic as every other 1D kernel (bitwise iterates); the residual sum is one
+// warp tree (history within the 1e-12 bar of the oracle, not bitwise equal to the multi-warp paths).
+// =============================================================================
+template <typename T, int C>
+__global__ void __launch_bounds__(32, 1)
+res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, int tpl, Ctrl* __restrict__ ctrl,
+             double* __restrict__ hist, long long hist_cap, double rdiv, double tol, int tol_mode,
+             double ref_residual, long long max_cycles, int k) {
+  constexpr int COL0 = 16 / sizeof(T);
+  constexpr bool FOLD = sizeof(T) == 8;
+  const int lane = threadIdx.x;
+  Ctrl cs = *ctrl;  // every lane keeps an identical copy (same inputs, same decisions)
+  if (cs.done) return;
+  const T* Xc = ((cs.c & 1) ? X1 : X0) + COL0;
+  T x[C], q[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    x[c] = Xc[C * lane + c];
+    q[c] = Q[C * lane + c];
+  }
+  const T ring_l = X0[COL0 - 1], ring_r = X0[COL0 + 32 * C];
+  const bool t0 = lane % tpl == 0, t1 = lane % tpl == tpl - 1;  // first / last lane of a tile
+  for (;;) {
+    const long long cyc = cs.c;
+    const int kk = cyc >= max_cycles ? 0 : k;
+    // frozen halo of x_c (the neighbouring tiles' edge points; the ring at the ends)
+    T hl = __shfl_up_sync(FULL, x[C - 1], 1);
+    T hr = __shfl_down_sync(FULL, x[0], 1);
+    if (lane == 0) hl = ring_l;
+    if (lane == 31) hr = ring_r;
+    // the snapshot x_c: in registers (C < 16), else written to X[c & 1] every cycle (fire-and-forget
+    // stores; the 32-point-per-lane case has no registers to spare)
+    constexpr bool SNAP_REG = C < 16;
+    T xs[SNAP_REG ? C : 1];
+    if constexpr (SNAP_REG) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) xs[c] = x[c];
+    } else {
+      T* Xd = ((cyc & 1) ? X1 : X0) + COL0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) Xd[C * lane + c] = x[c];
+    }
+    double acc = 0.0;
+    if (!FOLD || kk == 0) {
+      const T l = t0 ? hl : __shfl_up_sync(FULL, x[C - 1], 1);
+      const T r = t1 ? hr : __shfl_down_sync(FULL, x[0], 1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const T L = c == 0 ? l : x[c - 1];
+        const T R = c == C - 1 ? r : x[c + 1];
+        const double sv = res1((double)x[c], (double)L, (double)R, (double)(T(2) * q[c]));
+        acc = __fma_rn(sv, sv, acc);
+      }
+    }
+    int s = 0;
+    if constexpr (FOLD) {
+      if (kk > 0) {  // first sub-iteration: every lane's neighbours are x_c, i.e. exactly hl / hr
+        T prev = hl;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const T R = c == C - 1 ? hr : x[c + 1];
+          const double sum = __dadd_rn(prev, R);
+          const double t = __fma_rn(2.0, x[c], -sum);
+          const double rr = __fma_rn(2.0, q[c], -t);
+          acc = __fma_rn(rr, rr, acc);
+          prev = x[c];
+          x[c] = __fma_rn(0.5, sum, q[c]);
+        }
+        s = 1;
+      }
+    }
+#pragma unroll 1
+    for (; s < kk; ++s) {
+      T l = __shfl_up_sync(FULL, x[C - 1], 1);
+      T r = __shfl_down_sync(FULL, x[0], 1);
+      l = t0 ? hl : l;
+      r = t1 ? hr : r;
+      T prev = l;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const T R = c == C - 1 ? r : x[c + 1];
+        const T nv = upd1(prev, R, q[c]);
+        prev = x[c];
+        x[c] = nv;
+      }
+    }
+    const double S = __shfl_sync(FULL, warp_sum(acc), 0);  // one value for every lane
+    hj_decide(&cs, S, lane == 0 ? hist : nullptr, hist_cap, rdiv, tol, tol_mode, ref_residual, max_cycles);
+    if (cs.done) {  // x_c is the answer: into X[c & 1], where the engine extracts it
+      if constexpr (SNAP_REG) {
+        T* Xd = ((cyc & 1) ? X1 : X0) + COL0;
+#pragma unroll
+        for (int c = 0; c < C; ++c) Xd[C * lane + c] = xs[c];
+      }
+      break;
+    }
+  }
+  if (lane == 0) *ctrl = cs;
+}
+
+// =============================================================================
 // RES1DM — the resident 1D solver for MANY small tiles (tiles of 32 points, e.g. the paper's
 // 1024 copies of N = 1024 with T = 32: 32,768 tiles): each warp owns M consecutive tiles for the
 // whole solve, lane l holding point l of each, so a sub-iteration is M independent shuffle+update
@@ -702,6 +810,27 @@ cudaError_t launch_resident_1dm(const Geom& g, int M, void* X0, void* X1, const 
   }
 #undef HJ_RM
   return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, st);
+}
+
+// One small problem in one warp (res1w_kernel): ny == 1, nx = 32 C (C = 1..32), whole tiles of C-multiples.
+bool res1w_ok(const Geom& g) {
+  const long long C = g.nx / 32;
+  return g.dim == 1 && g.ny == 1 && !g.gen && g.omega == 1.0 && g.ox == 0 && g.nx % 32 == 0 && C >= 1 &&
+         C <= 32 && (C & (C - 1)) == 0 && g.tx % C == 0 && g.nx % g.tx == 0;
+}
+
+cudaError_t launch_resident_1w(const Geom& g, void* X0, void* X1, const void* Q, Ctrl* ctrl, double* hist,
+                               long long hist_cap, double tol, int tol_mode, double ref_residual,
+                               long long max_cycles, int k, cudaStream_t st) {
+  const int C = (int)(g.nx / 32), tpl = g.tx / C;
+  const bool f64 = g.dtype == HJ_F64;
+#define HJ_RW(CC)                                                                                            case CC:                                                                                                     if (f64)                                                                                                     res1w_kernel<double, CC><<<1, 32, 0, st>>>((double*)X0, (double*)X1, (const double*)Q, tpl, ctrl, hist,                                                  hist_cap, g.rdiv, tol, tol_mode, ref_residual, max_cycles, k);     else                                                                                                         res1w_kernel<float, CC><<<1, 32, 0, st>>>((float*)X0, (float*)X1, (const float*)Q, tpl, ctrl, hist,                                                     hist_cap, g.rdiv, tol, tol_mode, ref_residual, max_cycles, k);     break;
+  switch (C) {
+    HJ_RW(1) HJ_RW(2) HJ_RW(4) HJ_RW(8) HJ_RW(16) HJ_RW(32)
+    default: return cudaErrorInvalidValue;
+  }
+#undef HJ_RW
+  return cudaGetLastError();
 }
 
 cudaError_t launch_resident_1d(const Geom& g, void* X0, void* X1, const void* Q, double* part, Ctrl* ctrl,

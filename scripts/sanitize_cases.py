@@ -28,9 +28,23 @@ cases = [
     (2, 256, 128, dict(mode="hier", tile=(32, 32), k=6)),                # resident 2D (multi-CTA barrier)
     (1, 256, 1, dict(mode="hier", tile=32, k=16)),                      # resident 1D, one CTA
     (1, 4096, 2, dict(mode="hier", tile=128, k=5)),                     # resident 1D, multi-CTA
+    # round 2
+    (1, 1024, 1, dict(mode="hier", tile=32, k=5)),                      # resident 1D, one warp (res1w, C = 32)
+    (1, 256, 1, dict(mode="hier", tile=64, k=4, dtype="f32")),          # res1w, C = 8
+    (2, 96, 64, dict(mode="hier", tile=(16, 16), k=5)),                 # REGT: several tiles per warp
+    (2, 64, 96, dict(mode="hier", tile=(32, 16), k=4, dtype="f32")),
+    (2, 192, 96, dict(mode="hier", tile=(64, 32), k=5)),                # REGT: warp group per tile
+    (2, 128, 192, dict(mode="hier", tile=(64, 64), k=6)),
+    (2, 256, 96, dict(mode="hier", tile=(128, 32), k=3, dtype="f32")),
+    (2, 100, 70, dict(mode="hier", tile=(32, 32), k=5, overlap=(0, 4))),  # one-axis overlap
 ]
 for dim, nx, ny, kw in cases:
     p = make_problem("R", dim, nx, ny) if (dim == 2 or ny == 1) else make_problem("R", 1, nx, batch=ny)
     r = hj.jacobi_solve(dim, nx, ny, p["h"], p["f"], p["bc"], p["x0"], tol=1e-9, max_cycles=6, **kw)
     print(dim, nx, ny, kw, "cycles", r["cycles"], "status", r["status"])
+os.environ["HJ_RESIDENT"] = "0"   # the per-cycle path of a resident-eligible grid (run with HJ_SPLIT_CYCLE=1 too)
+for dim, nx, ny, kw in [(2, 128, 128, dict(mode="hier", tile=(32, 32), k=4))]:
+    p = make_problem("R", dim, nx, ny)
+    r = hj.jacobi_solve(dim, nx, ny, p["h"], p["f"], p["bc"], p["x0"], tol=1e-9, max_cycles=6, **kw)
+    print(dim, nx, ny, kw, "per-cycle", "cycles", r["cycles"], "status", r["status"])
 print("sanitize cases done")
