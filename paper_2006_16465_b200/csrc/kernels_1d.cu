@@ -392,8 +392,11 @@ res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
     }
     double acc = 0.0;
     if (!FOLD || kk == 0) {
-      const T l = t0 ? hl : __shfl_up_sync(FULL, x[C - 1], 1);
-      const T r = t1 ? hr : __shfl_down_sync(FULL, x[0], 1);
+      // (every lane shuffles; a shuffle inside a conditional expression would leave lanes out)
+      T l = __shfl_up_sync(FULL, x[C - 1], 1);
+      T r = __shfl_down_sync(FULL, x[0], 1);
+      l = t0 ? hl : l;
+      r = t1 ? hr : r;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         const T L = c == 0 ? l : x[c - 1];

@@ -10,15 +10,12 @@
 // weights held as kernel parameters; SK = 2: the Poisson update damped by omega (damp(), the
 // multigrid smoother of reading c24); SK = 0: the paper's Poisson update.  Everything else (tiles,
 // halo, stores) is unchanged.
-#include <cstdlib>
 #include <type_traits>
 
 #include "hj_internal.cuh"
 #include "reg_tile.cuh"
 
 namespace hj {
-
-bool reg2d_stream();
 
 namespace {
 
@@ -263,192 +260,6 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
         ax.n, ay.n, ty == 0 ? peer_lo : nullptr, ty == ay.nb - 1 && y0 + 32 == ay.n ? peer_hi : nullptr);
   }
   if (C::TMA_STORE && lane == 0) bulk_wait_all();
-}
-
-// =============================================================================
-// REG2DS — REG2D with the tile head streamed into the previous tile's last sub-iteration (the plain
-// case: o = 0, no multigrid correction / zero start, no TMA store).  Same cycle, same arithmetic, same
-// partials as reg2d_kernel; what moves is WHEN registers change hands: in a tile's last
-// sub-iteration every row, right after its new values are computed, is stored to the next iterate
-// (128-bit stores; the slab's first / last row also into the peer ghost rows) and its registers are
-// reloaded with the same row of the warp's NEXT tile from the shared-memory slot (already landed: its
-// TMA load was issued at this tile's head), so the slot -> register traffic and the stores overlap the
-// last sub-iteration's arithmetic instead of forming a separate tile head.  After the last
-// sub-iteration only the next tile's frozen halo is copied and the slot refilled.
-// =============================================================================
-template <typename T, typename C>
-struct StreamPost {
-  using V2 = typename VecOf<T>::v2;
-  T* gdst;              // interior origin of this tile in the next iterate
-  long long pitch;
-  const T* nsx;         // the next tile in the slot (nullptr: no next tile)
-  const T* nsf;
-  T* plo;               // peer ghost rows (row 0 / row 31 of the slab edge tiles) or nullptr
-  T* phi;
-  int x0, lx, ly;
-  template <typename TL>
-  __device__ __forceinline__ void row(TL& tl, int i, const T (&nw)[4]) const {
-    V2* dst = reinterpret_cast<V2*>(gdst + (8 * ly + i) * pitch + 4 * lx);
-    dst[0] = V2{nw[0], nw[1]};
-    dst[1] = V2{nw[2], nw[3]};
-    if (i == 0 && plo && ly == 0) {
-      V2* d = reinterpret_cast<V2*>(plo + x0 + 4 * lx);
-      d[0] = V2{nw[0], nw[1]};
-      d[1] = V2{nw[2], nw[3]};
-      __threadfence_system();
-    }
-    if (i == 7 && phi && ly == 3) {
-      V2* d = reinterpret_cast<V2*>(phi + x0 + 4 * lx);
-      d[0] = V2{nw[0], nw[1]};
-      d[1] = V2{nw[2], nw[3]};
-      __threadfence_system();
-    }
-    if (nsx) {
-      const int r = 8 * ly + i;
-      const V2* rowx = reinterpret_cast<const V2*>(nsx + (r + 1) * C::BW + C::COL0 + 4 * lx);
-      const V2* rowf = reinterpret_cast<const V2*>(nsf + r * 32 + 4 * lx);
-      const V2 a = rowx[0], b = rowx[1], fa = rowf[0], fb = rowf[1];
-      tl.x[i][0] = a.x; tl.x[i][1] = a.y; tl.x[i][2] = b.x; tl.x[i][3] = b.y;
-      tl.q[i][0] = fa.x; tl.q[i][1] = fa.y; tl.q[i][2] = fb.x; tl.q[i][3] = fb.y;
-    }
-  }
-};
-
-template <typename T, typename C, int SK>
-__global__ void __launch_bounds__(C::WARPS * 32, 1)
-reg2ds_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
-              T* __restrict__ xout, long long pitch, Axis ax, Axis ay, int ntx_full, long long nfull, int ntx,
-              double* __restrict__ part, const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt,
-              T* peer_lo, T* peer_hi, int ty0, int tys) {
-  using V2 = typename VecOf<T>::v2;
-  if (ctrl->done) return;
-  const int kk = (ctrl->c >= max_cycles) ? 0 : k;
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* base =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lx = lane & 7, ly = lane >> 3;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base) + warp;
-  unsigned char* slot = base + C::BARS + size_t(warp) * C::WSMEM;
-  const T* sx = reinterpret_cast<const T*>(slot);
-  const T* sf = reinterpret_cast<const T*>(slot + C::XSLOT);
-  T* hb = reinterpret_cast<T*>(slot + C::XSLOT + C::FBYTES + C::OBYTES);
-  const long long gw = (long long)blockIdx.x * C::WARPS + warp;
-  const long long nw = (long long)gridDim.x * C::WARPS;
-  if (gw >= nfull) return;
-  auto tile_xy = [&](long long u, int& tx, int& ty) {
-    tx = (int)(u % ntx_full);
-    ty = ty0 + (int)(u / ntx_full) * tys;
-  };
-  auto issue = [&](long long u) {
-    int tx, ty;
-    tile_xy(u, tx, ty);
-    mbar_arrive_expect_tx(bar, C::XBYTES + C::FBYTES);
-    tma_load_2d(slot, &tmX, axis_start(ax, tx), axis_start(ay, ty), bar);
-    tma_load_2d(slot + C::XSLOT, &tmF, axis_start(ax, tx), axis_start(ay, ty), bar);
-  };
-  if (lane == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-    prefetch_tensormap(&tmX);
-    prefetch_tensormap(&tmF);
-    issue(gw);
-  }
-  __syncwarp();
-  Tile2<T, false, SK> tl;
-  if constexpr (SK == 1) {
-    tl.cw[0] = (T)wt.w; tl.cw[1] = (T)wt.e; tl.cw[2] = (T)wt.s; tl.cw[3] = (T)wt.n;
-  }
-  if constexpr (SK == 2) tl.om = (T)wt.om;
-  tl.own = 0xffffffffu;
-  tl.hxp = hb + (lx == 0 ? 0 : 32) + 8 * ly;
-  tl.hyp = hb + (ly == 0 ? 64 : 96) + 4 * lx;
-  auto load_regs = [&] {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int r = 8 * ly + i;
-      const V2* rowx = reinterpret_cast<const V2*>(sx + (r + 1) * C::BW + C::COL0 + 4 * lx);
-      const V2* rowf = reinterpret_cast<const V2*>(sf + r * 32 + 4 * lx);
-      const V2 a = rowx[0], b = rowx[1], fa = rowf[0], fb = rowf[1];
-      tl.x[i][0] = a.x; tl.x[i][1] = a.y; tl.x[i][2] = b.x; tl.x[i][3] = b.y;
-      tl.q[i][0] = fa.x; tl.q[i][1] = fa.y; tl.q[i][2] = fb.x; tl.q[i][3] = fb.y;
-    }
-  };
-  mbar_wait(bar, 0);
-  load_regs();
-  int it = 0;
-  for (long long u = gw; u < nfull; u += nw, ++it) {
-    int tx, ty;
-    tile_xy(u, tx, ty);
-    const int x0 = axis_start(ax, tx), y0 = axis_start(ay, ty);
-    const bool has_next = u + nw < nfull;
-    // this tile's frozen halo (the slot still holds tile u: its x and q are in registers already)
-    hb[lane] = sx[(lane + 1) * C::BW + C::COL0 - 1];
-    hb[32 + lane] = sx[(lane + 1) * C::BW + C::COL0 + 32];
-    hb[64 + lane] = sx[C::COL0 + lane];
-    hb[96 + lane] = sx[33 * C::BW + C::COL0 + lane];
-    __syncwarp();
-    if (lane == 0 && has_next) {  // every value of the slot is in registers or the halo buffer
-      fence_proxy_async();
-      issue(u + nw);
-    }
-    StreamPost<T, C> post{xout + ((long long)y0 + 1) * pitch + C::COL0 + x0, pitch, nullptr, nullptr,
-                          ty == 0 ? peer_lo : nullptr, ty == ay.nb - 1 && y0 + 32 == ay.n ? peer_hi : nullptr,
-                          x0, lx, ly};
-    auto arm_next = [&] {  // the last sub-iteration streams the next tile in: its TMA load has landed
-      if (has_next) {
-        mbar_wait(bar, (it + 1) & 1);
-        post.nsx = sx;
-        post.nsf = sf;
-      }
-    };
-    constexpr bool FOLD = sizeof(T) == 8;
-    double acc = 0.0;
-    int s = 0;
-    if (FOLD && kk >= 8 && ((kk - 1) & 1)) {  // as reg2d_tile: residual sweep + plain sweep, then the reduction
-      double a4[4] = {0.0, 0.0, 0.0, 0.0};
-      tl.template sweep_mo<true>(lx, ly, a4);
-      tl.template sweep_mo<false>(lx, ly);
-      acc = warp_sum((a4[0] + a4[1]) + (a4[2] + a4[3]));
-      s = 2;
-    } else if (FOLD && kk == 1) {  // the residual sweep is also the last one
-      double a4[4] = {0.0, 0.0, 0.0, 0.0};
-      arm_next();
-      tl.template sweep_mo_p<true>(lx, ly, a4, post);
-      acc = warp_sum((a4[0] + a4[1]) + (a4[2] + a4[3]));
-      s = 1;
-    } else {
-      if (!FOLD || kk == 0) acc = tl.residual(lx, ly);
-      if (FOLD && kk > 0) {
-        double a4[4] = {0.0, 0.0, 0.0, 0.0};
-        tl.template sweep_mo<true>(lx, ly, a4);
-        acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-        s = 1;
-      }
-      acc = warp_sum(acc);
-    }
-    if (lane == 0) part[(long long)ty * ntx + tx] = acc;
-    if (kk == 0) {  // residual-only pass: no sub-iteration to stream the next tile into
-      if (has_next) {
-        mbar_wait(bar, (it + 1) & 1);
-        load_regs();
-      }
-      continue;
-    }
-    if (s < kk) {
-      // the middle sub-iterations (all but the last), an even number after an optional single one
-      if (((kk - 1 - s) & 1)) {
-        tl.template sweep_mo<false>(lx, ly);
-        ++s;
-      }
-#pragma unroll 1
-      for (; s < kk - 1; s += 2) {
-        tl.template sweep_mo<false>(lx, ly);
-        tl.template sweep_mo<false>(lx, ly);
-      }
-      arm_next();
-      tl.template sweep_mo_p<false>(lx, ly, nullptr, post);
-    }
-  }
 }
 
 // =============================================================================
@@ -838,13 +649,6 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
         }
       } else if (ovl) {
         go(R2<T>{}, std::true_type{}, X0{});
-      } else if (reg2d_stream()) {
-        using C = R2<T>;
-        long long ctas = (nfull + C::WARPS - 1) / C::WARPS;
-        if (ctas > grid_hint) ctas = grid_hint;
-        reg2ds_kernel<T, C, SK><<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
-            *a.tm_in, *a.tm_f, (T*)a.xout, g.pitch, g.ax, g.ay, (int)ntx_full, nfull, (int)g.ntx, a.part, a.ctrl,
-            g.k, a.max_cycles, wt, (T*)a.peer_lo, (T*)a.peer_hi, subset ? a.ty0 : 0, subset ? a.tys : 1);
       } else {
         go(R2<T>{}, std::false_type{}, X0{});
       }
@@ -871,19 +675,8 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
 }  // namespace
 
 
-// HJ_REG2D_STREAM=0 selects the round-1 kernel (the tile head as a separate phase) for A/B timing.
-bool reg2d_stream() {
-  static const bool on = [] { const char* e = std::getenv("HJ_REG2D_STREAM"); return !(e && e[0] == '0'); }();
-  return on;
-}
-
 template <typename T, typename C, int SK>
 cudaError_t cfg2() {
-  {
-    cudaError_t e0 = cudaFuncSetAttribute(reg2ds_kernel<T, C, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)C::SMEM);
-    if (e0 != cudaSuccess) return e0;
-  }
   cudaError_t e = cudaFuncSetAttribute(reg2d_kernel<T, C, false, SK>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   if (e != cudaSuccess) return e;

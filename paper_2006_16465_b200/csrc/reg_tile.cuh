@@ -181,19 +181,8 @@ struct Tile2 {
   // and 7 of the neighbouring lane rows) are consumed last, so consecutive sub-iterations overlap
   // instead of draining the pipeline.  The computed rows form a growing block [lo, hi]; the old
   // values of its two edge rows are kept in olo / ohi.
-  struct NoPost {
-    __device__ __forceinline__ void row(Tile2&, int, const T (&)[4]) const {}
-  };
   template <bool RES = false>
   __device__ __forceinline__ void sweep_mo(int lx, int ly, double* acc = nullptr) {
-    NoPost np;
-    sweep_mo_p<RES>(lx, ly, acc, np);
-  }
-  // sweep_mo with a per-row epilogue: post.row(*this, i, nw) right after row i got its new values
-  // (the last sub-iteration of a tile stores them and streams the next tile's row i into x[i], q[i]:
-  // nothing later in the sub-iteration reads x[i] — the old values of updated rows live in olo / ohi).
-  template <bool RES, typename Post>
-  __device__ __forceinline__ void sweep_mo_p(int lx, int ly, double* acc, Post& post) {
     T up[4], dn[4];
     exchange_ns(ly, up, dn);
     T olo[4], ohi[4];
@@ -234,7 +223,6 @@ struct Tile2 {
         else olo[c] = x[i][c];
         x[i][c] = nw[c];
       }
-      post.row(*this, i, nw);
     }
   }
 
