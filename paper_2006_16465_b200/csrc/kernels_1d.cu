@@ -9,6 +9,8 @@
 // (reading c23).  The kernels take SK (stencil kind): 0 the paper's Poisson update,
 // 1 the general coefficients (GEN), 2 the Poisson update damped by omega (damp(): the multigrid
 // smoother of reading c24).
+#include <type_traits>
+
 #include "hj_internal.cuh"
 
 namespace hj {
@@ -344,12 +346,20 @@ res1d_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, lo
 // RES1W — the resident solver for ONE small 1D problem (nx = 32 C <= 1024 points, e.g. BASELINE config
 // 1: N = 256, 8 tiles of 32, k = 16, tol 1e-8): the whole problem in ONE warp, C consecutive points
 // per lane, every tile a run of tx / C lanes.  No CTA barrier, no shared memory, no per-cycle global
-// traffic: per cycle the tile-edge lanes take the frozen halo of x_c by one shuffle each way, the k
-// sub-iterations run in registers (the first with the residual of x_c folded in, fp64), one warp
-// reduction and every lane takes the same stopping decision (hj_decide on the broadcast sum).  The
-// iterate x_c is kept beside x_{c+1} so that a converged solve returns the snapshot it tested.
-// Same per-point arithmetic as every other 1D kernel (bitwise iterates); the residual sum is one
-// warp tree (history within the 1e-12 bar of the oracle, not bitwise equal to the multi-warp paths).
+// traffic.  The cycle is a chain of dependent sub-iterations, so its time is the latency of that chain:
+//  * sub-iterations run in PAIRS with one exchange per pair: a lane also keeps the two points on each
+//    side of its own C (ghosts; the neighbouring lanes' points, their q preloaded), updates its C
+//    points and the inner ghost on each side in the pair's first sub-iteration and its C points in
+//    the second — one shuffle latency per two sub-iterations; the ghost updates are the same
+//    expression of the same values as in the neighbour (bitwise the same iterate); at a tile edge the
+//    ghost is the frozen halo of x_c and is not updated;
+//  * the residual of x_c is folded into the first sub-iteration (fp64) and its warp reduction is
+//    spread over the following pairs (one butterfly step per pair), so only the stopping decision
+//    (hj_decide on the broadcast sum, the same on every lane) is left at the end of the cycle;
+//  * x_c is kept beside x_{c+1} (registers for C < 16, else stored each cycle) so a converged solve
+//    returns the snapshot it tested.
+// Same per-point arithmetic as every other 1D kernel (bitwise iterates); the residual sum is one warp
+// tree (history within the 1e-12 bar of the oracle, not bitwise equal to the multi-warp paths).
 // =============================================================================
 template <typename T, int C>
 __global__ void __launch_bounds__(32, 1)
@@ -370,6 +380,8 @@ res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
   }
   const T ring_l = X0[COL0 - 1], ring_r = X0[COL0 + 32 * C];
   const bool t0 = lane % tpl == 0, t1 = lane % tpl == tpl - 1;  // first / last lane of a tile
+  // q of the inner ghosts (the neighbours' edge points): constant for the whole solve
+  const T qgl = __shfl_up_sync(FULL, q[C - 1], 1), qgr = __shfl_down_sync(FULL, q[0], 1);
   for (;;) {
     const long long cyc = cs.c;
     const int kk = cyc >= max_cycles ? 0 : k;
@@ -378,8 +390,7 @@ res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
     T hr = __shfl_down_sync(FULL, x[0], 1);
     if (lane == 0) hl = ring_l;
     if (lane == 31) hr = ring_r;
-    // the snapshot x_c: in registers (C < 16), else written to X[c & 1] every cycle (fire-and-forget
-    // stores; the 32-point-per-lane case has no registers to spare)
+    // the snapshot x_c: in registers (C < 16), else written to X[c & 1] every cycle
     constexpr bool SNAP_REG = C < 16;
     T xs[SNAP_REG ? C : 1];
     if constexpr (SNAP_REG) {
@@ -391,53 +402,79 @@ res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
       for (int c = 0; c < C; ++c) Xd[C * lane + c] = x[c];
     }
     double acc = 0.0;
-    if (!FOLD || kk == 0) {
-      // (every lane shuffles; a shuffle inside a conditional expression would leave lanes out)
-      T l = __shfl_up_sync(FULL, x[C - 1], 1);
-      T r = __shfl_down_sync(FULL, x[0], 1);
-      l = t0 ? hl : l;
-      r = t1 ? hr : r;
+    if (!FOLD || kk == 0) {  // separate residual pass of x_c (fp32, residual-only cycle)
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        const T L = c == 0 ? l : x[c - 1];
-        const T R = c == C - 1 ? r : x[c + 1];
+        const T L = c == 0 ? hl : x[c - 1];
+        const T R = c == C - 1 ? hr : x[c + 1];
         const double sv = res1((double)x[c], (double)L, (double)R, (double)(T(2) * q[c]));
         acc = __fma_rn(sv, sv, acc);
       }
     }
-    int s = 0;
-    if constexpr (FOLD) {
-      if (kk > 0) {  // first sub-iteration: every lane's neighbours are x_c, i.e. exactly hl / hr
-        T prev = hl;
+    // one sub-iteration of the own points, neighbours L (left of point 0) and R (right of point C-1);
+    // RES: fold the residual of the current values (x_c) in
+    auto sweep1 = [&](T L, T R, auto res) {
+      T prev = L;
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-          const T R = c == C - 1 ? hr : x[c + 1];
-          const double sum = __dadd_rn(prev, R);
+      for (int c = 0; c < C; ++c) {
+        const T Rc = c == C - 1 ? R : x[c + 1];
+        if constexpr (decltype(res)::value) {
+          const double sum = __dadd_rn(prev, Rc);
           const double t = __fma_rn(2.0, x[c], -sum);
           const double rr = __fma_rn(2.0, q[c], -t);
           acc = __fma_rn(rr, rr, acc);
           prev = x[c];
           x[c] = __fma_rn(0.5, sum, q[c]);
+        } else {
+          const T nv = upd1(prev, Rc, q[c]);
+          prev = x[c];
+          x[c] = nv;
         }
-        s = 1;
       }
+    };
+    // two sub-iterations with one exchange: ghosts at -2, -1 (left) and C, C+1 (right)
+    // (C >= 2: the inner ghost's other neighbour is in the same lane, hence in the same tile; C == 1
+    // runs single sub-iterations with one exchange each)
+    auto pair = [&](auto res) {
+      T g1 = __shfl_up_sync(FULL, x[C - 1], 1), g2 = __shfl_up_sync(FULL, x[C >= 2 ? C - 2 : 0], 1);
+      T h0 = __shfl_down_sync(FULL, x[0], 1), h1 = __shfl_down_sync(FULL, x[C >= 2 ? 1 : 0], 1);
+      g1 = t0 ? hl : g1;
+      h0 = t1 ? hr : h0;
+      if constexpr (C >= 2) {
+        // first sub-iteration: the inner ghosts too (not at a tile edge, where they are the frozen halo)
+        const T gn = t0 ? hl : upd1(g2, x[0], qgl);
+        const T hn = t1 ? hr : upd1(x[C - 1], h1, qgr);
+        sweep1(g1, h0, res);
+        sweep1(gn, hn, std::false_type{});
+      } else {
+        sweep1(g1, h0, res);
+        T l = __shfl_up_sync(FULL, x[0], 1), r = __shfl_down_sync(FULL, x[0], 1);
+        l = t0 ? hl : l;
+        r = t1 ? hr : r;
+        sweep1(l, r, std::false_type{});
+      }
+    };
+    int s = 0;
+    if (kk & 1) {  // an odd count: one single sub-iteration first (the fold, fp64)
+      if constexpr (FOLD) sweep1(hl, hr, std::true_type{});
+      else sweep1(hl, hr, std::false_type{});
+      s = 1;
+    } else if (kk > 0) {
+      if constexpr (FOLD) pair(std::true_type{});
+      else pair(std::false_type{});
+      s = 2;
     }
+    int step = 16;  // butterfly of acc, one step per following pair
 #pragma unroll 1
-    for (; s < kk; ++s) {
-      T l = __shfl_up_sync(FULL, x[C - 1], 1);
-      T r = __shfl_down_sync(FULL, x[0], 1);
-      l = t0 ? hl : l;
-      r = t1 ? hr : r;
-      T prev = l;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const T R = c == C - 1 ? r : x[c + 1];
-        const T nv = upd1(prev, R, q[c]);
-        prev = x[c];
-        x[c] = nv;
+    for (; s < kk; s += 2) {
+      pair(std::false_type{});
+      if (step) {
+        acc += __shfl_xor_sync(FULL, acc, step);
+        step >>= 1;
       }
     }
-    const double S = __shfl_sync(FULL, warp_sum(acc), 0);  // one value for every lane
+    for (; step; step >>= 1) acc += __shfl_xor_sync(FULL, acc, step);
+    const double S = __shfl_sync(FULL, acc, 0);  // one value for every lane
     hj_decide(&cs, S, lane == 0 ? hist : nullptr, hist_cap, rdiv, tol, tol_mode, ref_residual, max_cycles);
     if (cs.done) {  // x_c is the answer: into X[c & 1], where the engine extracts it
       if constexpr (SNAP_REG) {

@@ -45,6 +45,9 @@ CASES = [
     ("R", 1, 1024, 1, dict(tile=32, k=5, tol=0.0, max_cycles=9)),                # C = 32, one lane per tile
     ("R", 1, 512, 1, dict(tile=128, k=3, tol=0.0, max_cycles=8, dtype="f32")),   # C = 16, snapshot in HBM
     ("R", 1, 64, 1, dict(tile=64, k=4, tol=0.0, max_cycles=6)),                  # C = 2, one tile
+    ("R", 1, 32, 1, dict(tile=32, k=6, tol=0.0, max_cycles=5)),                  # C = 1: unpaired sub-iterations
+    ("R", 1, 256, 1, dict(tile=64, k=9, tol=0.0, max_cycles=7)),                 # odd k: one single, then pairs
+    ("R", 1, 512, 1, dict(tile=32, k=2, tol=0.0, max_cycles=5, dtype="f32")),    # C = 16, f32 residual pass
     ("P", 1, 1024, 1, dict(tile=32, k=16, tol=1e-6, max_cycles=10**6)),          # the paper's single N = 1024
 ]
 
