@@ -380,6 +380,13 @@ res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
   }
   const T ring_l = X0[COL0 - 1], ring_r = X0[COL0 + 32 * C];
   const bool t0 = lane % tpl == 0, t1 = lane % tpl == tpl - 1;  // first / last lane of a tile
+  const long long c_first = cs.c;
+  double thr = tol * cs.sqrtS0, lo2, hi2;  // the relative stopping threshold (set at c = 0 or on resume)
+  {
+    const double t2 = thr * thr;
+    lo2 = t2 * (1.0 - 0x1p-49);
+    hi2 = t2 * (1.0 + 0x1p-49);
+  }
   // q of the inner ghosts (the neighbours' edge points): constant for the whole solve
   const T qgl = __shfl_up_sync(FULL, q[C - 1], 1), qgr = __shfl_down_sync(FULL, q[0], 1);
   for (;;) {
@@ -475,7 +482,38 @@ res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
     }
     for (; step; step >>= 1) acc += __shfl_xor_sync(FULL, acc, step);
     const double S = __shfl_sync(FULL, acc, 0);  // one value for every lane
-    hj_decide(&cs, S, lane == 0 ? hist : nullptr, hist_cap, rdiv, tol, tol_mode, ref_residual, max_cycles);
+    // the history gets S itself now and sqrt(S) / rdiv after the loop (the same value hj_decide would
+    // write), keeping the square root and the division off the per-cycle chain
+    if (lane == 0 && hist && cyc < hist_cap) hist[cyc] = S;
+    if (cyc == 0 || tol_mode != 0) {
+      hj_decide(&cs, S, nullptr, hist_cap, rdiv, tol, tol_mode, ref_residual, max_cycles);
+      thr = tol * cs.sqrtS0;
+      const double t2 = thr * thr;
+      lo2 = t2 * (1.0 - 0x1p-49);
+      hi2 = t2 * (1.0 + 0x1p-49);
+    } else {
+      // relative test sqrt(S) <= thr (hj_decide, reading c1) decided without the square root unless S is
+      // within a few ulps of thr^2: S < lo2 implies sqrt(S) < thr exactly, S > hi2 implies RN(sqrt(S)) > thr
+      cs.S_last = S;
+      const bool conv = S < lo2 ? true : (S > hi2 ? false : sqrt(S) <= thr);
+      if (!isfinite(S)) {
+        cs.status = HJ_ERR_NUMERIC;
+        cs.done = 1;
+        cs.c_done = cyc;
+      } else if (conv) {
+        cs.done = 1;
+        cs.converged = 1;
+        cs.status = HJ_OK;
+        cs.c_done = cyc;
+      } else if (cyc >= max_cycles) {
+        cs.done = 1;
+        cs.converged = 0;
+        cs.status = HJ_NOT_CONVERGED;
+        cs.c_done = cyc;
+      } else {
+        cs.c = cyc + 1;
+      }
+    }
     if (cs.done) {  // x_c is the answer: into X[c & 1], where the engine extracts it
       if constexpr (SNAP_REG) {
         T* Xd = ((cyc & 1) ? X1 : X0) + COL0;
@@ -484,6 +522,11 @@ res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
       }
       break;
     }
+  }
+  if (hist) {  // S -> sqrt(S) / rdiv for the entries this launch wrote
+    __syncwarp();
+    const long long last = cs.c_done < hist_cap - 1 ? cs.c_done : hist_cap - 1;
+    for (long long i = c_first + lane; i <= last; i += 32) hist[i] = sqrt(hist[i]) / rdiv;
   }
   if (lane == 0) *ctrl = cs;
 }
