@@ -10,12 +10,19 @@
 // weights held as kernel parameters; SK = 2: the Poisson update damped by omega (damp(), the
 // multigrid smoother of reading c24); SK = 0: the paper's Poisson update.  Everything else (tiles,
 // halo, stores) is unchanged.
+#include <cstdlib>
 #include <type_traits>
 
 #include "hj_internal.cuh"
 #include "reg_tile.cuh"
 
 namespace hj {
+
+// HJ_TILE_STRIP=S: REG2D walks the tiles in column strips of S tiles (0 / unset: row-major)
+static int tile_strip() {
+  static const int sw = [] { const char* e = std::getenv("HJ_TILE_STRIP"); return e ? std::atoi(e) : 0; }();
+  return sw;
+}
 
 namespace {
 
@@ -201,7 +208,7 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
              const __grid_constant__ CUtensorMap tmO, T* __restrict__ xout, long long pitch,
              Axis ax, Axis ay, int ntx_full, long long nfull, int ntx, double* __restrict__ part,
              const Ctrl* __restrict__ ctrl, int k, long long max_cycles, Wt2 wt,
-             const __grid_constant__ CUtensorMap tmE, T* peer_lo, T* peer_hi, int ty0, int tys) {
+             const __grid_constant__ CUtensorMap tmE, T* peer_lo, T* peer_hi, int ty0, int tys, int sw) {
   if (ctrl->done) return;
   constexpr bool COR = XM == 1, ZX = XM == 2;
   const int kk = (ctrl->c >= max_cycles) ? 0 : k;
@@ -219,8 +226,23 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
   const long long gw = (long long)blockIdx.x * C::WARPS + warp;
   const long long nw = (long long)gridDim.x * C::WARPS;
   if (gw >= nfull) return;
+  // u -> tile: row-major (sw == 0), or column strips of sw tiles walked row by row (sw > 0, sw divides
+  // ntx_full; HJ_TILE_STRIP, an experiment on L2 / TLB locality)
+  const long long nrows_t = nfull / ntx_full;
+  auto tile_of = [&](long long u, int& tx, int& ty) {
+    if (sw > 0) {
+      const long long per = (long long)sw * nrows_t, st = u / per, r = u % per;
+      tx = (int)(st * sw + r % sw);
+      ty = ty0 + (int)(r / sw) * tys;
+    } else {
+      tx = (int)(u % ntx_full);
+      ty = ty0 + (int)(u / ntx_full) * tys;
+    }
+  };
   auto issue = [&](long long u) {  // u: full-block index; box origin = block's interior origin
-    const int cx = axis_start(ax, (int)(u % ntx_full)), cy = axis_start(ay, ty0 + (int)(u / ntx_full) * tys);
+    int utx, uty;
+    tile_of(u, utx, uty);
+    const int cx = axis_start(ax, utx), cy = axis_start(ay, uty);
     mbar_arrive_expect_tx(bar, (ZX ? 0 : C::XBYTES) + C::FBYTES + (COR ? C::EBYTES : 0));
     if (!ZX) tma_load_2d(slot, &tmX, cx, cy, bar);    // x box: padded rows 32ty.., cols 32tx..
     tma_load_2d(slot + C::XSLOT, &tmF, cx, cy, bar);   // h2f box
@@ -239,7 +261,8 @@ reg2d_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
   int it = 0;
   for (long long u = gw; u < nfull; u += nw, ++it) {
     mbar_wait(bar, it & 1);
-    const int tx = (int)(u % ntx_full), ty = ty0 + (int)(u / ntx_full) * tys;
+    int tx, ty;
+    tile_of(u, tx, ty);
     const int x0 = axis_start(ax, tx), y0 = axis_start(ay, ty);
     reg2d_tile<T, C, MASK, SK, XM>(
         wt, sx, sf, so, hb, lane, kk, part, (long long)ty * ntx + tx,
@@ -631,7 +654,8 @@ cudaError_t launch_2d_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaSt
             <<<(unsigned)ctas, C::WARPS * 32, C::SMEM, st>>>(
                 *a.tm_in, *a.tm_f, *a.tm_out, (T*)a.xout, g.pitch, g.ax, g.ay, (int)ntx_full, nfull,
                 (int)g.ntx, a.part, a.ctrl, g.k, a.max_cycles, wt, a.tm_cor ? *a.tm_cor : *a.tm_in,
-                (T*)a.peer_lo, (T*)a.peer_hi, subset ? a.ty0 : 0, subset ? a.tys : 1);
+                (T*)a.peer_lo, (T*)a.peer_hi, subset ? a.ty0 : 0, subset ? a.tys : 1,
+                (!subset && tile_strip() > 0 && ntx_full % tile_strip() == 0) ? tile_strip() : 0);
       };
       using X0 = std::integral_constant<int, 0>;
       using X1 = std::integral_constant<int, 1>;
