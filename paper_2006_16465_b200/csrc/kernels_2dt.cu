@@ -19,6 +19,8 @@
 //    sub-iteration's values of its in-tile neighbours and the frozen snapshot outside the tile.
 // Poisson, o = 0, nx and ny multiples of max(Tx, 32) / max(Ty, 32) (engine.cu choose_kernel);
 // everything else runs on smem2d_kernel.
+#include <cstdlib>
+
 #include "hj_internal.cuh"
 #include "reg_tile.cuh"
 
@@ -147,7 +149,7 @@ template <typename T, int TX, int TY>
 __global__ void __launch_bounds__(RT<T, TX, TY>::WARPS * 32, 1)
 regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
             T* __restrict__ xout, long long pitch, long long nunits, int units_x, double* __restrict__ part,
-            long long ppr, const Ctrl* __restrict__ ctrl, int k, long long max_cycles) {
+            long long ppr, const Ctrl* __restrict__ ctrl, int k, long long max_cycles, int sweep_bar) {
   using R = RT<T, TX, TY>;
   using C = typename R::C;
   using V2 = typename VecOf<T>::v2;
@@ -288,6 +290,7 @@ regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
           double a4[4] = {0.0, 0.0, 0.0, 0.0};
           setup(0);
           tl.template sweep_h<true>(lx, ly, a4, ex);
+          if (sweep_bar) group_bar(bar_id, bar_n);
           acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
           s = 1;
         }
@@ -297,6 +300,7 @@ regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         setup(s);
         tl.template sweep_h<false>(lx, ly, nullptr, ex);
         if (s > 0) ph ^= 1u << (s & 1);  // this parity's mbarriers completed one more phase
+        if (sweep_bar) group_bar(bar_id, bar_n);
       }
     }
     // residual partials: per tile (small tiles: segmented reduction over the tile's lanes)
@@ -328,6 +332,14 @@ regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   }
 }
 
+// HJ_REGT_SWEEP_BARRIER=1 (diagnostics): a group barrier after every sub-iteration of a large tile, on top
+// of the mbarrier exchange — the ordering racecheck models (it does not follow mbarrier arrive / wait
+// between warps); same values, slower.
+bool regt_sweep_barrier() {
+  static const bool on = [] { const char* e = std::getenv("HJ_REGT_SWEEP_BARRIER"); return e && e[0] == '1'; }();
+  return on;
+}
+
 template <typename T, int TX, int TY>
 cudaError_t launch_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
   using R = RT<T, TX, TY>;
@@ -337,7 +349,7 @@ cudaError_t launch_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStrea
   if (ctas > grid_hint) ctas = grid_hint;
   regt_kernel<T, TX, TY><<<(unsigned)ctas, R::WARPS * 32, R::SMEM, st>>>(
       *a.tm_in, *a.tm_f, (T*)a.xout, g.pitch, nunits, (int)units_x, a.part, g.parts_per_row, a.ctrl, g.k,
-      a.max_cycles);
+      a.max_cycles, regt_sweep_barrier() ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -11,3 +11,7 @@ for tool in memcheck racecheck synccheck initcheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_cases.py > gpurun_out/sanitize_final_$tool.log 2>&1
   echo "$tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' gpurun_out/sanitize_final_$tool.log | tail -1)"
 done
+# the REGT large-tile hazards racecheck reports are mbarrier-ordered (it does not model mbarrier arrive/wait
+# between warps): the same cases with a group barrier after every sub-iteration
+HJ_REGT_SWEEP_BARRIER=1 timeout 900 compute-sanitizer --tool racecheck --print-limit 20 python scripts/sanitize_cases.py > gpurun_out/sanitize_final_racecheck_sweepbar.log 2>&1
+echo "racecheck (sweep barrier) rc=$? $(grep -E 'RACECHECK SUMMARY|ERROR SUMMARY' gpurun_out/sanitize_final_racecheck_sweepbar.log | tail -1)"
