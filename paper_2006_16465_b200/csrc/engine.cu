@@ -1070,6 +1070,15 @@ static hj_status run_resident(hj_plan* P, bool* used) {
   }
   const int k = g.k;
   cudaError_t e;
+  int rc_c = 0, rc_d = 0;
+  if (res1c_ok(g, &rc_c, &rc_d)) {
+    // one small 1D problem: the whole solve in one CTA (res1c_kernel)
+    e = launch_resident_1c(g, rc_c, rc_d, P->X[0], P->X[1], P->H2F, P->ctrl, P->hist, P->hist_cap, P->prm.tol,
+                           (int)P->prm.tol_mode, P->prm.ref_residual, P->prm.max_cycles, k, P->stream);
+    HJ_CUDA(e);
+    *used = true;
+    return HJ_OK;
+  }
   if (res1w_ok(g) && !(std::getenv("HJ_RES1W") && std::getenv("HJ_RES1W")[0] == '0')) {
     // one small 1D problem: the whole solve in one warp (res1w_kernel)
     e = launch_resident_1w(g, P->X[0], P->X[1], P->H2F, P->ctrl, P->hist, P->hist_cap, P->prm.tol,

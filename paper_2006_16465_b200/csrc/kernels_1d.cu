@@ -9,6 +9,8 @@
 // (reading c23).  The kernels take SK (stencil kind): 0 the paper's Poisson update,
 // 1 the general coefficients (GEN), 2 the Poisson update damped by omega (damp(): the multigrid
 // smoother of reading c24).
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "hj_internal.cuh"
@@ -532,6 +534,209 @@ res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
 }
 
 // =============================================================================
+// RES1C — the resident solver for ONE small 1D problem spread over one CTA: W = nx / (32 C) <= 8 warps
+// (one per scheduler for W = 4), C consecutive points per lane, every tile a run of tpl = tx / C lanes
+// inside one warp.  Same cycle as RES1W (§4.1: frozen halo of x_c, k sub-iterations,
+// the residual of x_c folded into the first), but the k-long chain of dependent sub-iterations runs
+// on W schedulers instead of one, and the exchange between lanes happens once per GROUP of D
+// sub-iterations: a lane keeps D ghost points on each side (the neighbouring lanes' points, their q
+// preloaded) and in the group's j-th sub-iteration updates its C points and the D - j inner ghosts
+// on each side — the ghost updates are the neighbour's own expression on the same values, so the
+// iterate is bitwise that of every other 1D kernel.  A ghost that is the tile's frozen halo (ghost
+// -m with m == p C + 1 for the lane at position p of its tile) keeps its value; ghosts beyond it
+// carry values of the next tile that never reach the tile (the frozen ghost separates them).
+// Between warps: each cycle every warp publishes its edge points of x_{c+1} and its residual partial
+// in shared memory (slots by cycle parity), ONE __syncthreads, then every thread sums the W partials
+// in warp order and takes the same decision (the history within the 1e-12 bar of the oracle).
+// =============================================================================
+template <typename T, int C, int D>
+__global__ void __launch_bounds__(256, 1)
+res1c_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, int nx, int tpl,
+             Ctrl* __restrict__ ctrl, double* __restrict__ hist, long long hist_cap, double rdiv, double tol,
+             int tol_mode, double ref_residual, long long max_cycles, int k) {
+  constexpr int COL0 = 16 / sizeof(T);
+  constexpr bool FOLD = sizeof(T) == 8;
+  __shared__ T s_e[2][8][2];    // [cycle parity][warp][first, last point] of the iterate entering the cycle
+  __shared__ double s_p[2][8];  // [cycle parity][warp] residual partial
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+  Ctrl cs = *ctrl;  // every thread keeps an identical copy (same inputs, same decisions)
+  if (cs.done) return;
+  const T* Xc = ((cs.c & 1) ? X1 : X0) + COL0;
+  T x[C], q[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    x[c] = Xc[C * threadIdx.x + c];
+    q[c] = Q[C * threadIdx.x + c];
+  }
+  const T ring_l = X0[COL0 - 1], ring_r = X0[COL0 + nx];
+  const int p = lane % tpl, tf = lane - p, tl = tf + tpl - 1;  // position in the tile, its first / last lane
+  bool fl[D], fr[D];  // ghost m (1-based) is the tile's frozen left / right halo
+  T qgl[D], qgr[D];   // q at the ghosts (constant for the whole solve)
+#pragma unroll
+  for (int m = 1; m <= D; ++m) {
+    fl[m - 1] = m == p * C + 1;
+    fr[m - 1] = m == (tpl - 1 - p) * C + 1;
+    qgl[m - 1] = __shfl_up_sync(FULL, q[C - 1 - (m - 1) % C], (m - 1) / C + 1);
+    qgr[m - 1] = __shfl_down_sync(FULL, q[(m - 1) % C], (m - 1) / C + 1);
+  }
+  const long long c_first = cs.c;
+  double thr = tol * cs.sqrtS0, lo2, hi2;  // the relative stopping threshold (set at c = 0 or on resume)
+  {
+    const double t2 = thr * thr;
+    lo2 = t2 * (1.0 - 0x1p-49);
+    hi2 = t2 * (1.0 + 0x1p-49);
+  }
+  if (lane == 0) s_e[cs.c & 1][w][0] = x[0];
+  if (lane == 31) s_e[cs.c & 1][w][1] = x[C - 1];
+  __syncthreads();
+  T gl[D], gr[D];  // ghosts: gl[m-1] = point -m, gr[m-1] = point C-1+m
+  for (;;) {
+    const long long cyc = cs.c;
+    const int par = (int)(cyc & 1);
+    const int kk = cyc >= max_cycles ? 0 : k;
+    // the tiles' frozen halo of x_c: the neighbouring tile's edge point (another warp's: shared memory)
+    T hl = __shfl_sync(FULL, x[C - 1], (tf - 1) & 31);
+    T hr = __shfl_sync(FULL, x[0], (tl + 1) & 31);
+    if (tf == 0) hl = w > 0 ? s_e[par][w - 1][1] : ring_l;
+    if (tl == 31) hr = w < W - 1 ? s_e[par][w + 1][0] : ring_r;
+    T xs[C];  // the snapshot x_c (returned if the cycle's test stops the solve)
+#pragma unroll
+    for (int c = 0; c < C; ++c) xs[c] = x[c];
+    // ghosts of depth d from the neighbouring lanes; the frozen ones take the halo
+    auto exch = [&](auto dd) {
+      constexpr int d = decltype(dd)::value;
+#pragma unroll
+      for (int m = 1; m <= d; ++m) {
+        const T a = __shfl_up_sync(FULL, x[C - 1 - (m - 1) % C], (m - 1) / C + 1);
+        const T b = __shfl_down_sync(FULL, x[(m - 1) % C], (m - 1) / C + 1);
+        gl[m - 1] = fl[m - 1] ? hl : a;
+        gr[m - 1] = fr[m - 1] ? hr : b;
+      }
+    };
+    double acc = 0.0;
+    if (!FOLD || kk == 0) {  // separate residual pass of x_c (fp32, residual-only cycle)
+      exch(std::integral_constant<int, 1>{});
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const T L = c == 0 ? gl[0] : x[c - 1];
+        const T R = c == C - 1 ? gr[0] : x[c + 1];
+        const double sv = res1((double)x[c], (double)L, (double)R, (double)(T(2) * q[c]));
+        acc = __fma_rn(sv, sv, acc);
+      }
+    }
+    // a group of d sub-iterations after one exchange; RES: fold the residual of x_c into the first
+    auto group = [&](auto dd, auto res) {
+      constexpr int d = decltype(dd)::value;
+      exch(dd);
+#pragma unroll
+      for (int j = 1; j <= d; ++j) {
+        const int e = d - j;  // ghosts still valid after this sub-iteration
+        T ngl[D > 1 ? D - 1 : 1], ngr[D > 1 ? D - 1 : 1], nv[C];
+#pragma unroll
+        for (int m = 1; m <= e; ++m) {
+          ngl[m - 1] = fl[m - 1] ? gl[m - 1] : upd1(gl[m], m == 1 ? x[0] : gl[m - 2], qgl[m - 1]);
+          ngr[m - 1] = fr[m - 1] ? gr[m - 1] : upd1(m == 1 ? x[C - 1] : gr[m - 2], gr[m], qgr[m - 1]);
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const T L = c == 0 ? gl[0] : x[c - 1];
+          const T R = c == C - 1 ? gr[0] : x[c + 1];
+          if constexpr (decltype(res)::value) {
+            if (j == 1) {
+              const double sum = __dadd_rn(L, R);
+              const double t = __fma_rn(2.0, x[c], -sum);
+              const double rr = __fma_rn(2.0, q[c], -t);
+              acc = __fma_rn(rr, rr, acc);
+              nv[c] = __fma_rn(0.5, sum, q[c]);
+              continue;
+            }
+          }
+          nv[c] = upd1(L, R, q[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) x[c] = nv[c];
+#pragma unroll
+        for (int m = 1; m <= e; ++m) {
+          gl[m - 1] = ngl[m - 1];
+          gr[m - 1] = ngr[m - 1];
+        }
+      }
+    };
+    using I1 = std::integral_constant<int, 1>;
+    using ID = std::integral_constant<int, D>;
+    int s = 0;
+    const int rem = kk % D;
+    if (rem) {  // k not a multiple of D: single sub-iterations first (the first one folds)
+      if constexpr (FOLD) group(I1{}, std::true_type{});
+      else group(I1{}, std::false_type{});
+      for (s = 1; s < rem; ++s) group(I1{}, std::false_type{});
+    } else if (kk > 0) {
+      if constexpr (FOLD) group(ID{}, std::true_type{});
+      else group(ID{}, std::false_type{});
+      s = D;
+    }
+    int step = 16;  // butterfly of acc, one step per following group
+#pragma unroll 1
+    for (; s < kk; s += D) {
+      group(ID{}, std::false_type{});
+      if (step) {
+        acc += __shfl_xor_sync(FULL, acc, step);
+        step >>= 1;
+      }
+    }
+    for (; step; step >>= 1) acc += __shfl_xor_sync(FULL, acc, step);
+    if (lane == 0) {
+      s_p[par][w] = acc;
+      s_e[par ^ 1][w][0] = x[0];
+    }
+    if (lane == 31) s_e[par ^ 1][w][1] = x[C - 1];
+    __syncthreads();
+    double S = s_p[par][0];
+    for (int v = 1; v < W; ++v) S += s_p[par][v];
+    if (threadIdx.x == 0 && hist && cyc < hist_cap) hist[cyc] = S;
+    if (cyc == 0 || tol_mode != 0) {
+      hj_decide(&cs, S, nullptr, hist_cap, rdiv, tol, tol_mode, ref_residual, max_cycles);
+      thr = tol * cs.sqrtS0;
+      const double t2 = thr * thr;
+      lo2 = t2 * (1.0 - 0x1p-49);
+      hi2 = t2 * (1.0 + 0x1p-49);
+    } else {  // as RES1W: the relative test without the square root away from the threshold
+      cs.S_last = S;
+      const bool conv = S < lo2 ? true : (S > hi2 ? false : sqrt(S) <= thr);
+      if (!isfinite(S)) {
+        cs.status = HJ_ERR_NUMERIC;
+        cs.done = 1;
+        cs.c_done = cyc;
+      } else if (conv) {
+        cs.done = 1;
+        cs.converged = 1;
+        cs.status = HJ_OK;
+        cs.c_done = cyc;
+      } else if (cyc >= max_cycles) {
+        cs.done = 1;
+        cs.converged = 0;
+        cs.status = HJ_NOT_CONVERGED;
+        cs.c_done = cyc;
+      } else {
+        cs.c = cyc + 1;
+      }
+    }
+    if (cs.done) {  // x_c is the answer: into X[c & 1], where the engine extracts it
+      T* Xd = ((cyc & 1) ? X1 : X0) + COL0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) Xd[C * threadIdx.x + c] = xs[c];
+      break;
+    }
+  }
+  if (hist) {  // S -> sqrt(S) / rdiv for the entries this launch wrote
+    __syncthreads();
+    const long long last = cs.c_done < hist_cap - 1 ? cs.c_done : hist_cap - 1;
+    for (long long i = c_first + threadIdx.x; i <= last; i += blockDim.x) hist[i] = sqrt(hist[i]) / rdiv;
+  }
+  if (threadIdx.x == 0) *ctrl = cs;
+}
+
+// =============================================================================
 // RES1DM — the resident 1D solver for MANY small tiles (tiles of 32 points, e.g. the paper's
 // 1024 copies of N = 1024 with T = 32: 32,768 tiles): each warp owns M consecutive tiles for the
 // whole solve, lane l holding point l of each, so a sub-iteration is M independent shuffle+update
@@ -914,6 +1119,49 @@ cudaError_t launch_resident_1w(const Geom& g, void* X0, void* X1, const void* Q,
   }
 #undef HJ_RW
   return cudaGetLastError();
+}
+
+// One small problem in one CTA (res1c_kernel): C points per lane, W = nx / (32 C) <= 8 warps, tiles of
+// tpl = tx / C lanes inside a warp (tpl a power of two <= 32).  *C / *D: the layout (RES1C_C, RES1C_D
+// defaults, HJ_RES1C="C,D" overrides, HJ_RES1C=0 disables).
+bool res1c_ok(const Geom& g, int* C, int* D) {
+  int c = RES1C_C, d = RES1C_D;
+  if (const char* s = std::getenv("HJ_RES1C")) {
+    if (s[0] == '0') return false;
+    if (std::sscanf(s, "%d,%d", &c, &d) != 2) return false;
+  }
+  if (!(c == 1 || c == 2 || c == 4 || c == 8) || !(d == 1 || d == 2 || d == 4)) return false;
+  if (!(g.dim == 1 && g.ny == 1 && !g.gen && g.omega == 1.0 && g.ox == 0)) return false;
+  if (g.nx % (32LL * c) || g.nx / (32LL * c) > 8 || g.tx % c || g.nx % g.tx) return false;
+  const long long tpl = g.tx / c;
+  if (tpl > 32 || (tpl & (tpl - 1))) return false;
+  *C = c;
+  *D = d;
+  return true;
+}
+
+cudaError_t launch_resident_1c(const Geom& g, int C, int D, void* X0, void* X1, const void* Q, Ctrl* ctrl,
+                               double* hist, long long hist_cap, double tol, int tol_mode, double ref_residual,
+                               long long max_cycles, int k, cudaStream_t st) {
+  const int nx = (int)g.nx, tpl = (int)g.tx / C, threads = nx / C;
+  const bool f64 = g.dtype == HJ_F64;
+  double rdiv = g.rdiv;
+#define HJ_RC(CC, DD)                                                                                  \
+  if (C == CC && D == DD) {                                                                            \
+    if (f64)                                                                                           \
+      res1c_kernel<double, CC, DD><<<1, threads, 0, st>>>((double*)X0, (double*)X1, (const double*)Q,  \
+                                                          nx, tpl, ctrl, hist, hist_cap, rdiv, tol,    \
+                                                          tol_mode, ref_residual, max_cycles, k);      \
+    else                                                                                               \
+      res1c_kernel<float, CC, DD><<<1, threads, 0, st>>>((float*)X0, (float*)X1, (const float*)Q, nx,  \
+                                                         tpl, ctrl, hist, hist_cap, rdiv, tol,         \
+                                                         tol_mode, ref_residual, max_cycles, k);       \
+    return cudaGetLastError();                                                                         \
+  }
+  HJ_RC(1, 1) HJ_RC(1, 2) HJ_RC(1, 4) HJ_RC(2, 1) HJ_RC(2, 2) HJ_RC(2, 4)
+  HJ_RC(4, 1) HJ_RC(4, 2) HJ_RC(4, 4) HJ_RC(8, 1) HJ_RC(8, 2) HJ_RC(8, 4)
+#undef HJ_RC
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_resident_1d(const Geom& g, void* X0, void* X1, const void* Q, double* part, Ctrl* ctrl,
