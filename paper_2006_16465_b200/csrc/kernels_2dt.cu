@@ -72,13 +72,29 @@ __device__ __forceinline__ void sts2(uint32_t a, double x, double y) {
 __device__ __forceinline__ void sts2(uint32_t a, float x, float y) {
   asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x), "f"(y) : "memory");
 }
+// predicated (branch-free) form: lanes with p == 0 issue nothing
+__device__ __forceinline__ void sts2p(bool p, uint32_t a, double x, double y) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\n@q st.shared.v2.f64 [%0], {%1, %2};\n}" ::"r"(a), "d"(x),
+               "d"(y), "r"((int)p)
+               : "memory");
+}
+__device__ __forceinline__ void sts2p(bool p, uint32_t a, float x, float y) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\n@q st.shared.v2.f32 [%0], {%1, %2};\n}" ::"r"(a), "f"(x),
+               "f"(y), "r"((int)p)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_u32(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
 // All addresses are 32-bit shared-window addresses derived from the warp index (few live registers):
 //   halo buffer of warp w, parity p:  hb0 + w * WSMEM + p * (HX + HY) * sizeof(T)
 //   halo mbarrier (w, p, half):       mb0 + 8 * (4 w + 2 p + half)
-template <typename T, typename R>
+// XCH (exchange mode of the large tiles): 0 — the mbarrier scheme above, sends as divergent branches;
+// 2 — no mbarriers: the sends are predicated stores and the tile's warps meet at ONE named barrier
+// (bar.sync, hardware, no polling loop) after every sub-iteration (the parity buffers make one
+// barrier per sub-iteration enough: a buffer read in sub-iteration s is rewritten in s + 1 by a
+// neighbour that has passed the barrier ending s); 3 — the mbarrier scheme with predicated sends.
+template <typename T, typename R, int XCH = 0>
 struct Exch {
   uint32_t hb0, mb0;      // shared addresses: halo buffer of warp 0, halo mbarrier (0, 0, 0)
   int warp, lx, ly, lane;
@@ -89,11 +105,34 @@ struct Exch {
     return hb0 + (uint32_t)(w * R::WSMEM) + (uint32_t)(pw * (R::HX + R::HY) * (int)sizeof(T));
   }
   __device__ __forceinline__ uint32_t mbar(int w, int half) const { return mb0 + 8u * (4 * w + 2 * pw + half); }
-  __device__ __forceinline__ void wait_a() const { if (do_wait && (hW || hE)) mbar_wait_u32(wa, wph); }
-  __device__ __forceinline__ void wait_b() const { if (do_wait) mbar_wait_u32(wb, wph); }
+  __device__ __forceinline__ void wait_a() const {
+    if constexpr (XCH != 2)
+      if (do_wait && (hW || hE)) mbar_wait_u32(wa, wph);
+  }
+  __device__ __forceinline__ void wait_b() const {
+    if constexpr (XCH != 2)
+      if (do_wait) mbar_wait_u32(wb, wph);
+  }
   template <typename TL>
   __device__ __forceinline__ void send_a(const TL& t) const {
     if (!do_send) return;
+    if constexpr (XCH != 0) {
+      constexpr uint32_t E = sizeof(T);
+      const bool pw_ = hW && lx == 0, pe_ = hE && lx == 7;
+      const uint32_t qw = halo(warp - 1) + (7 * 32 + 8 * ly) * E, qe = halo(warp + 1) + (8 * ly) * E;
+      sts2p(pw_, qw + 2 * E, t.x[2][0], t.x[3][0]);
+      sts2p(pw_, qw + 4 * E, t.x[4][0], t.x[5][0]);
+      sts2p(pe_, qe + 2 * E, t.x[2][3], t.x[3][3]);
+      sts2p(pe_, qe + 4 * E, t.x[4][3], t.x[5][3]);
+      if constexpr (XCH == 3) {
+        __syncwarp();
+        if (lane == 0) {
+          if (hW) mbar_arrive_u32(mbar(warp - 1, 0));
+          if (hE) mbar_arrive_u32(mbar(warp + 1, 0));
+        }
+      }
+      return;
+    }
     constexpr uint32_t E = sizeof(T);
     if (hW && lx == 0) {  // my column 0 -> W neighbour's E column (its lane-column 7)
       const uint32_t q = halo(warp - 1) + (7 * 32 + 8 * ly) * E;
@@ -114,6 +153,31 @@ struct Exch {
   template <typename TL>
   __device__ __forceinline__ void send_b(const TL& t) const {
     if (!do_send) return;
+    if constexpr (XCH != 0) {
+      constexpr uint32_t E = sizeof(T);
+      const bool pw_ = hW && lx == 0, pe_ = hE && lx == 7, ps_ = hS && ly == 0, pn_ = hN && ly == 3;
+      const uint32_t qw = halo(warp - 1) + (7 * 32 + 8 * ly) * E, qe = halo(warp + 1) + (8 * ly) * E;
+      const uint32_t qs = halo(warp - R::SBX) + (R::HX + 3 * 32 + 4 * lx) * E;
+      const uint32_t qn = halo(warp + R::SBX) + (R::HX + 4 * lx) * E;
+      sts2p(pw_, qw, t.x[0][0], t.x[1][0]);
+      sts2p(pw_, qw + 6 * E, t.x[6][0], t.x[7][0]);
+      sts2p(pe_, qe, t.x[0][3], t.x[1][3]);
+      sts2p(pe_, qe + 6 * E, t.x[6][3], t.x[7][3]);
+      sts2p(ps_, qs, t.x[0][0], t.x[0][1]);
+      sts2p(ps_, qs + 2 * E, t.x[0][2], t.x[0][3]);
+      sts2p(pn_, qn, t.x[7][0], t.x[7][1]);
+      sts2p(pn_, qn + 2 * E, t.x[7][2], t.x[7][3]);
+      if constexpr (XCH == 3) {
+        __syncwarp();
+        if (lane == 0) {
+          if (hW) mbar_arrive_u32(mbar(warp - 1, 1));
+          if (hE) mbar_arrive_u32(mbar(warp + 1, 1));
+          if (hS) mbar_arrive_u32(mbar(warp - R::SBX, 1));
+          if (hN) mbar_arrive_u32(mbar(warp + R::SBX, 1));
+        }
+      }
+      return;
+    }
     constexpr uint32_t E = sizeof(T);
     if (hW && lx == 0) {
       const uint32_t q = halo(warp - 1) + (7 * 32 + 8 * ly) * E;
@@ -145,7 +209,7 @@ struct Exch {
   }
 };
 
-template <typename T, int TX, int TY>
+template <typename T, int TX, int TY, int XCH = 0>
 __global__ void __launch_bounds__(RT<T, TX, TY>::WARPS * 32, 1)
 regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
             T* __restrict__ xout, long long pitch, long long nunits, int units_x, double* __restrict__ part,
@@ -268,7 +332,7 @@ regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
 #pragma unroll 1
       for (; s < kk; ++s) tl.template sweep_mo<false>(lx, ly);
     } else {
-      Exch<T, R> ex;
+      Exch<T, R, XCH> ex;
       ex.hb0 = smem_u32(halo_of(0));
       ex.mb0 = smem_u32(hmb(0, 0, 0));
       ex.warp = warp; ex.lx = lx; ex.ly = ly; ex.lane = lane;
@@ -290,7 +354,7 @@ regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
           double a4[4] = {0.0, 0.0, 0.0, 0.0};
           setup(0);
           tl.template sweep_h<true>(lx, ly, a4, ex);
-          if (sweep_bar) group_bar(bar_id, bar_n);
+          if (XCH == 2 || sweep_bar) group_bar(bar_id, bar_n);
           acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
           s = 1;
         }
@@ -300,7 +364,7 @@ regt_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         setup(s);
         tl.template sweep_h<false>(lx, ly, nullptr, ex);
         if (s > 0) ph ^= 1u << (s & 1);  // this parity's mbarriers completed one more phase
-        if (sweep_bar) group_bar(bar_id, bar_n);
+        if (XCH == 2 || sweep_bar) group_bar(bar_id, bar_n);
       }
     }
     // residual partials: per tile (small tiles: segmented reduction over the tile's lanes)
@@ -339,6 +403,16 @@ bool regt_sweep_barrier() {
   static const bool on = [] { const char* e = std::getenv("HJ_REGT_SWEEP_BARRIER"); return e && e[0] == '1'; }();
   return on;
 }
+// HJ_REGT_XCH = 0 / 2 / 3: the large tiles' exchange mode (Exch); default REGT_XCH
+constexpr int REGT_XCH = 0;
+int regt_xch() {
+  static const int m = [] {
+    const char* e = std::getenv("HJ_REGT_XCH");
+    const int v = e ? std::atoi(e) : REGT_XCH;
+    return (v == 2 || v == 3) ? v : 0;
+  }();
+  return m;
+}
 
 template <typename T, int TX, int TY>
 cudaError_t launch_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStream_t st) {
@@ -347,16 +421,27 @@ cudaError_t launch_t(const Geom& g, const CycleArgs& a, int grid_hint, cudaStrea
   const long long nunits = R::BIG ? units_x * (g.ny / TY) : units_x * (g.ny / 32);
   long long ctas = (nunits + R::GROUPS - 1) / R::GROUPS;
   if (ctas > grid_hint) ctas = grid_hint;
-  regt_kernel<T, TX, TY><<<(unsigned)ctas, R::WARPS * 32, R::SMEM, st>>>(
-      *a.tm_in, *a.tm_f, (T*)a.xout, g.pitch, nunits, (int)units_x, a.part, g.parts_per_row, a.ctrl, g.k,
-      a.max_cycles, regt_sweep_barrier() ? 1 : 0);
+  const int xch = R::BIG && !regt_sweep_barrier() ? regt_xch() : 0;
+  auto fn = xch == 2 ? regt_kernel<T, TX, TY, (R::BIG ? 2 : 0)>
+                     : xch == 3 ? regt_kernel<T, TX, TY, (R::BIG ? 3 : 0)> : regt_kernel<T, TX, TY, 0>;
+  fn<<<(unsigned)ctas, R::WARPS * 32, R::SMEM, st>>>(*a.tm_in, *a.tm_f, (T*)a.xout, g.pitch, nunits, (int)units_x,
+                                                    a.part, g.parts_per_row, a.ctrl, g.k, a.max_cycles,
+                                                    regt_sweep_barrier() ? 1 : 0);
   return cudaGetLastError();
 }
 
 template <typename T, int TX, int TY>
 cudaError_t cfg_t() {
-  return cudaFuncSetAttribute(regt_kernel<T, TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)RT<T, TX, TY>::SMEM);
+  constexpr bool BIG = RT<T, TX, TY>::BIG;
+  cudaError_t e = cudaFuncSetAttribute(regt_kernel<T, TX, TY, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)RT<T, TX, TY>::SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(regt_kernel<T, TX, TY, (BIG ? 2 : 0)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)RT<T, TX, TY>::SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(regt_kernel<T, TX, TY, (BIG ? 3 : 0)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)RT<T, TX, TY>::SMEM);
+  return e;
 }
 
 template <typename T>
