@@ -153,7 +153,7 @@ cudaError_t launch_resident_1dm(const Geom& g, int M, void* X0, void* X1, const 
                                 double ref_residual, long long max_cycles, int k, unsigned int* bar, cudaStream_t st);
 bool res1w_ok(const Geom& g);
 // res1c: one small 1D problem in one CTA (C points per lane, ghost depth D); default layout
-constexpr int RES1C_C = 2, RES1C_D = 2;
+constexpr int RES1C_C = 8, RES1C_D = 4;
 bool res1c_ok(const Geom& g, int* C, int* D);
 cudaError_t launch_resident_1c(const Geom& g, int C, int D, void* X0, void* X1, const void* Q, Ctrl* ctrl,
                                double* hist, long long hist_cap, double tol, int tol_mode, double ref_residual,

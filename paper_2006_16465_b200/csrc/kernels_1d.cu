@@ -1126,10 +1126,15 @@ cudaError_t launch_resident_1w(const Geom& g, void* X0, void* X1, const void* Q,
 // defaults, HJ_RES1C="C,D" overrides, HJ_RES1C=0 disables).
 bool res1c_ok(const Geom& g, int* C, int* D) {
   int c = RES1C_C, d = RES1C_D;
+  bool forced = false;
   if (const char* s = std::getenv("HJ_RES1C")) {
     if (s[0] == '0') return false;
     if (std::sscanf(s, "%d,%d", &c, &d) != 2) return false;
+    forced = true;
   }
+  // by default only where res1w would hold >= 16 points per lane (nx >= 512): measured faster there
+  // (1D N = 1024: 1.38 vs 2.42 us per cycle), slower at config 1 (N = 256: 1.20 vs 1.14 us)
+  if (!forced && g.nx < 512) return false;
   if (!(c == 1 || c == 2 || c == 4 || c == 8) || !(d == 1 || d == 2 || d == 4)) return false;
   if (!(g.dim == 1 && g.ny == 1 && !g.gen && g.omega == 1.0 && g.ox == 0)) return false;
   if (g.nx % (32LL * c) || g.nx / (32LL * c) > 8 || g.tx % c || g.nx % g.tx) return false;

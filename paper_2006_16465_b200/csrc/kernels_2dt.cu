@@ -14,8 +14,10 @@
 //  * large tiles (Tx, Ty >= 32; 64x32, 32x64, 64x64, 128x32): one tile = a group of
 //    (Tx/32) x (Ty/32) warps of one CTA, each holding one block; after every sub-iteration the
 //    warps of a tile write their block-edge rows / columns into the neighbouring warps' halo
-//    buffers (double-buffered by sub-iteration parity) and meet at a named barrier; tile edges keep
-//    the frozen halo.  The iterate is exactly the method's: every cell sees the previous
+//    buffers (double-buffered by sub-iteration parity, predicated stores) and meet at a named
+//    barrier (exchange mode 2, the default; the half-sub-iteration mbarrier scheme, modes 0 / 3, is
+//    kept for A/B: 5-12% slower at k = 4 and 16, profiles/r02_regt_xch.md); tile edges keep the
+//    frozen halo.  The iterate is exactly the method's: every cell sees the previous
 //    sub-iteration's values of its in-tile neighbours and the frozen snapshot outside the tile.
 // Poisson, o = 0, nx and ny multiples of max(Tx, 32) / max(Ty, 32) (engine.cu choose_kernel);
 // everything else runs on smem2d_kernel.
@@ -404,7 +406,7 @@ bool regt_sweep_barrier() {
   return on;
 }
 // HJ_REGT_XCH = 0 / 2 / 3: the large tiles' exchange mode (Exch); default REGT_XCH
-constexpr int REGT_XCH = 0;
+constexpr int REGT_XCH = 2;
 int regt_xch() {
   static const int m = [] {
     const char* e = std::getenv("HJ_REGT_XCH");

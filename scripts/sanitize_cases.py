@@ -42,6 +42,14 @@ for dim, nx, ny, kw in cases:
     p = make_problem("R", dim, nx, ny) if (dim == 2 or ny == 1) else make_problem("R", 1, nx, batch=ny)
     r = hj.jacobi_solve(dim, nx, ny, p["h"], p["f"], p["bc"], p["x0"], tol=1e-9, max_cycles=6, **kw)
     print(dim, nx, ny, kw, "cycles", r["cycles"], "status", r["status"])
+for lay in ("1,4", "4,2", "8,1", "2,1", "0"):  # res1c layouts (C, D); "0" = res1w
+    os.environ["HJ_RES1C"] = lay
+    for dim, nx, ny, kw in [(1, 256, 1, dict(mode="hier", tile=32, k=7)),
+                            (1, 256, 1, dict(mode="hier", tile=64, k=4, dtype="f32"))]:
+        p = make_problem("R", dim, nx, ny)
+        r = hj.jacobi_solve(dim, nx, ny, p["h"], p["f"], p["bc"], p["x0"], tol=1e-9, max_cycles=6, **kw)
+        print(dim, nx, ny, kw, "HJ_RES1C", lay, "cycles", r["cycles"], "status", r["status"])
+os.environ.pop("HJ_RES1C")
 os.environ["HJ_RESIDENT"] = "0"   # the per-cycle path of a resident-eligible grid (run with HJ_SPLIT_CYCLE=1 too)
 for dim, nx, ny, kw in [(2, 128, 128, dict(mode="hier", tile=(32, 32), k=4))]:
     p = make_problem("R", dim, nx, ny)

@@ -23,6 +23,8 @@ CASES = [
     ("R", 64, dict(tile=4, k=7, tol=0.0, max_cycles=6)),                         # tiles narrower than D ghosts
     ("R", 256, dict(tile=256, k=1, tol=0.0, max_cycles=4)),                      # k < D, one tile
     ("R", 256, dict(tile=32, k=4, tol=0.0, max_cycles=0)),                       # residual-only cycle
+    ("R", 2048, dict(tile=256, k=6, tol=0.0, max_cycles=4)),                     # eight warps of C = 8
+    ("P", 1024, dict(tile=32, k=16, tol=1e-6, max_cycles=10**6)),                # the paper's single N = 1024
 ]
 
 
