@@ -26,6 +26,53 @@ __global__ void chain(double* out, int iters, double a, long long* clk) {
   out[threadIdx.x] = v + f;
 }
 
+// res1w-like cycle (C = 8 points per lane, tiles of 4 lanes, k = 16 as 8 pairs, residual butterfly
+// spread over the pairs, a uniform decision per cycle): cycles per solver cycle
+__global__ void res1w_like(double* out, int cycles, long long* clk) {
+  const unsigned F = 0xffffffffu;
+  const int lane = threadIdx.x;
+  double x[8], q[8];
+  for (int c = 0; c < 8; ++c) { x[c] = 1.0 + lane * 8 + c; q[c] = 1e-3 * c; }
+  const bool t0 = lane % 4 == 0, t1 = lane % 4 == 3;
+  const double qgl = __shfl_up_sync(F, q[7], 1), qgr = __shfl_down_sync(F, q[0], 1);
+  double tot = 0.0;
+  long long t_0 = clock64();
+  for (int cyc = 0; cyc < cycles; ++cyc) {
+    double hl = __shfl_up_sync(F, x[7], 1), hr = __shfl_down_sync(F, x[0], 1);
+    double acc = 0.0;
+    int step = 16;
+#pragma unroll 1
+    for (int s = 0; s < 16; s += 2) {
+      double g1 = __shfl_up_sync(F, x[7], 1), g2 = __shfl_up_sync(F, x[6], 1);
+      double h0 = __shfl_down_sync(F, x[0], 1), h1 = __shfl_down_sync(F, x[1], 1);
+      g1 = t0 ? hl : g1;
+      h0 = t1 ? hr : h0;
+      const double gn = t0 ? hl : __fma_rn(0.5, __dadd_rn(g2, x[0]), qgl);
+      const double hn = t1 ? hr : __fma_rn(0.5, __dadd_rn(x[7], h1), qgr);
+      for (int pass = 0; pass < 2; ++pass) {
+        double prev = pass ? gn : g1;
+        const double R = pass ? hn : h0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const double Rc = c == 7 ? R : x[c + 1];
+          const double nv = __fma_rn(0.5, __dadd_rn(prev, Rc), q[c]);
+          if (s == 0 && pass == 0) acc = __fma_rn(nv, nv, acc);
+          prev = x[c];
+          x[c] = nv;
+        }
+      }
+      if (step) { acc += __shfl_xor_sync(F, acc, step); step >>= 1; }
+    }
+    for (; step; step >>= 1) acc += __shfl_xor_sync(F, acc, step);
+    const double S = __shfl_sync(F, acc, 0);
+    tot += S;
+    if (S < -1.0) break;  // uniform, never taken
+  }
+  long long t_1 = clock64();
+  if (lane == 0) *clk = t_1 - t_0;
+  out[lane] = tot + x[0];
+}
+
 int main() {
   double* out; long long* clk;
   cudaMalloc(&out, 1024 * sizeof(double));
@@ -49,6 +96,24 @@ int main() {
       cudaMemcpy(&c, clk, sizeof(c), cudaMemcpyDeviceToHost);
     }
     printf("%-32s %.2f cycles per link\n", names[op], (double)c / iters);
+  }
+  {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    long long c = 0;
+    const int cycles = 20000;
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(e0);
+      res1w_like<<<1, 32>>>(out, cycles, clk);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      cudaMemcpy(&c, clk, sizeof(c), cudaMemcpyDeviceToHost);
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("%-32s %.1f cycles per solver cycle, %.3f us per solver cycle, effective SM clock %.0f MHz\n",
+           "res1w-like cycle (C=8, k=16)", (double)c / cycles, ms * 1e3 / cycles, (double)c / (ms * 1e3));
   }
   return 0;
 }
