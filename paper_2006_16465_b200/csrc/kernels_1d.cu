@@ -363,7 +363,7 @@ res1d_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, lo
 // Same per-point arithmetic as every other 1D kernel (bitwise iterates); the residual sum is one warp
 // tree (history within the 1e-12 bar of the oracle, not bitwise equal to the multi-warp paths).
 // =============================================================================
-template <typename T, int C>
+template <typename T, int C, int U = 2>
 __global__ void __launch_bounds__(32, 1)
 res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, int tpl, Ctrl* __restrict__ ctrl,
              double* __restrict__ hist, long long hist_cap, double rdiv, double tol, int tol_mode,
@@ -391,12 +391,33 @@ res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
   }
   // q of the inner ghosts (the neighbours' edge points): constant for the whole solve
   const T qgl = __shfl_up_sync(FULL, q[C - 1], 1), qgr = __shfl_down_sync(FULL, q[0], 1);
+  // PIPE (C >= 4): the exchange is software-pipelined — the shuffles a pair needs (the neighbours'
+  // two edge points each side) are issued at the END of the previous pair, in the same basic block
+  // as its interior updates, so their latency overlaps arithmetic instead of heading the next pair
+  // (ncu of the unpipelined loop: the shuffle -> first-DADD wait and the butterfly's shuffle -> DADD
+  // wait were the top stalls, in-order issue blocking the warp behind each); the shuffles issued
+  // after a cycle's last pair are the next cycle's first exchange AND its frozen halo.
+  constexpr bool PIPE = C >= 4;
+  T sg1, sg2, sh0, sh1;  // pending: left lane's x[C-1], x[C-2]; right lane's x[0], x[1]
+  auto issue = [&] {
+    sg1 = __shfl_up_sync(FULL, x[C - 1], 1);
+    sg2 = __shfl_up_sync(FULL, x[C >= 2 ? C - 2 : 0], 1);
+    sh0 = __shfl_down_sync(FULL, x[0], 1);
+    sh1 = __shfl_down_sync(FULL, x[C >= 2 ? 1 : 0], 1);
+  };
+  if constexpr (PIPE) issue();
   for (;;) {
     const long long cyc = cs.c;
     const int kk = cyc >= max_cycles ? 0 : k;
     // frozen halo of x_c (the neighbouring tiles' edge points; the ring at the ends)
-    T hl = __shfl_up_sync(FULL, x[C - 1], 1);
-    T hr = __shfl_down_sync(FULL, x[0], 1);
+    T hl, hr;
+    if constexpr (PIPE) {
+      hl = sg1;
+      hr = sh0;
+    } else {
+      hl = __shfl_up_sync(FULL, x[C - 1], 1);
+      hr = __shfl_down_sync(FULL, x[0], 1);
+    }
     if (lane == 0) hl = ring_l;
     if (lane == 31) hr = ring_r;
     // the snapshot x_c: in registers (C < 16), else written to X[c & 1] every cycle
@@ -445,8 +466,8 @@ res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
     // (C >= 2: the inner ghost's other neighbour is in the same lane, hence in the same tile; C == 1
     // runs single sub-iterations with one exchange each)
     auto pair = [&](auto res) {
-      T g1 = __shfl_up_sync(FULL, x[C - 1], 1), g2 = __shfl_up_sync(FULL, x[C >= 2 ? C - 2 : 0], 1);
-      T h0 = __shfl_down_sync(FULL, x[0], 1), h1 = __shfl_down_sync(FULL, x[C >= 2 ? 1 : 0], 1);
+      if constexpr (!PIPE) issue();
+      T g1 = sg1, g2 = sg2, h0 = sh0, h1 = sh1;
       g1 = t0 ? hl : g1;
       h0 = t1 ? hr : h0;
       if constexpr (C >= 2) {
@@ -455,6 +476,7 @@ res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
         const T hn = t1 ? hr : upd1(x[C - 1], h1, qgr);
         sweep1(g1, h0, res);
         sweep1(gn, hn, std::false_type{});
+        if constexpr (PIPE) issue();  // the next pair's exchange (or the next cycle's halo)
       } else {
         sweep1(g1, h0, res);
         T l = __shfl_up_sync(FULL, x[0], 1), r = __shfl_down_sync(FULL, x[0], 1);
@@ -467,20 +489,22 @@ res1w_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
     if (kk & 1) {  // an odd count: one single sub-iteration first (the fold, fp64)
       if constexpr (FOLD) sweep1(hl, hr, std::true_type{});
       else sweep1(hl, hr, std::false_type{});
+      if constexpr (PIPE) issue();
       s = 1;
     } else if (kk > 0) {
       if constexpr (FOLD) pair(std::true_type{});
       else pair(std::false_type{});
       s = 2;
     }
-    int step = 16;  // butterfly of acc, one step per following pair
-#pragma unroll 1
+    int step = 16;  // butterfly of acc, one step per following pair: its shuffle issued before the
+                    // pair and its add predicated after it (no branch, no wait inside the pair);
+                    // two pairs per loop body so ptxas sees one pair's shuffles feed the next
+#pragma unroll U
     for (; s < kk; s += 2) {
+      const double pb = __shfl_xor_sync(FULL, acc, step ? step : 16);
       pair(std::false_type{});
-      if (step) {
-        acc += __shfl_xor_sync(FULL, acc, step);
-        step >>= 1;
-      }
+      acc = step ? acc + pb : acc;
+      step >>= 1;
     }
     for (; step; step >>= 1) acc += __shfl_xor_sync(FULL, acc, step);
     const double S = __shfl_sync(FULL, acc, 0);  // one value for every lane
@@ -1112,7 +1136,20 @@ cudaError_t launch_resident_1w(const Geom& g, void* X0, void* X1, const void* Q,
                                long long max_cycles, int k, cudaStream_t st) {
   const int C = (int)(g.nx / 32), tpl = g.tx / C;
   const bool f64 = g.dtype == HJ_F64;
-#define HJ_RW(CC)                                                                                            case CC:                                                                                                     if (f64)                                                                                                     res1w_kernel<double, CC><<<1, 32, 0, st>>>((double*)X0, (double*)X1, (const double*)Q, tpl, ctrl, hist,                                                  hist_cap, g.rdiv, tol, tol_mode, ref_residual, max_cycles, k);     else                                                                                                         res1w_kernel<float, CC><<<1, 32, 0, st>>>((float*)X0, (float*)X1, (const float*)Q, tpl, ctrl, hist,                                                     hist_cap, g.rdiv, tol, tol_mode, ref_residual, max_cycles, k);     break;
+  // HJ_RES1W_UNROLL=1: the pair loop not unrolled (A/B of the software-pipelined exchange)
+  static const bool u1 = [] { const char* e = std::getenv("HJ_RES1W_UNROLL"); return e && e[0] == '1'; }();
+#define HJ_RW(CC)                                                                                    \
+  case CC:                                                                                           \
+    if (f64) {                                                                                       \
+      auto fn = u1 ? res1w_kernel<double, CC, 1> : res1w_kernel<double, CC, 2>;                      \
+      fn<<<1, 32, 0, st>>>((double*)X0, (double*)X1, (const double*)Q, tpl, ctrl, hist, hist_cap,    \
+                           g.rdiv, tol, tol_mode, ref_residual, max_cycles, k);                       \
+    } else {                                                                                         \
+      auto fn = u1 ? res1w_kernel<float, CC, 1> : res1w_kernel<float, CC, 2>;                        \
+      fn<<<1, 32, 0, st>>>((float*)X0, (float*)X1, (const float*)Q, tpl, ctrl, hist, hist_cap,       \
+                           g.rdiv, tol, tol_mode, ref_residual, max_cycles, k);                       \
+    }                                                                                                \
+    break;
   switch (C) {
     HJ_RW(1) HJ_RW(2) HJ_RW(4) HJ_RW(8) HJ_RW(16) HJ_RW(32)
     default: return cudaErrorInvalidValue;
