@@ -592,6 +592,12 @@ def main():
                 "basis": "power-law fit of measured cycles-to-1e-6 at 2048^2, 4096^2 and 8192^2 (8192^2: "
                          "2,991,978 cycles, 1465 s measured; profiles/r01_convergence_scaling.json, "
                          "r01_convergence_8192.json) x the measured cycle time"}
+        part = os.path.join(ROOT, "profiles", "r02_ttt_1e-6_16384_partial.json")
+        if os.path.exists(part):  # the measured start of the same solve (resumed segments, one B200)
+            pd = json.load(open(part))["reached"]
+            proj["measured_partial"] = {"cycles": pd["cycles"], "seconds_device": pd["seconds_device"],
+                                        "rel_residual": pd["rel"], "lower_bound": True,
+                                        "source": "profiles/r02_ttt_1e-6_16384_partial.json"}
         if classic_ms:
             ccyc = fit["classic"]["cycles_16384"]
             proj["classic_sweeps_projected"] = ccyc
