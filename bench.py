@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -593,11 +594,29 @@ def main():
                          "2,991,978 cycles, 1465 s measured; profiles/r01_convergence_scaling.json, "
                          "r01_convergence_8192.json) x the measured cycle time"}
         part = os.path.join(ROOT, "profiles", "r02_ttt_1e-6_16384_partial.json")
+        kap = os.path.join(ROOT, "profiles", "r02_smooth_rate.json")
         if os.path.exists(part):  # the measured start of the same solve (resumed segments, one B200)
-            pd = json.load(open(part))["reached"]
+            pj = json.load(open(part))
+            pd = pj["reached"]
             proj["measured_partial"] = {"cycles": pd["cycles"], "seconds_device": pd["seconds_device"],
                                         "rel_residual": pd["rel"], "lower_bound": True,
                                         "source": "profiles/r02_ttt_1e-6_16384_partial.json"}
+            if os.path.exists(kap):
+                # the rest bracketed by the last measured segment's decay rate (faster) and the cycle's
+                # computed asymptotic smooth-mode rate kappa * (-ln cos(pi h)) (slower), both measured /
+                # computed independently of the power-law fit above
+                tr = pj["trajectory"]
+                r_last = -math.log(tr[-1]["rel"] / tr[-2]["rel"]) / (tr[-1]["cycles"] - tr[-2]["cycles"])
+                r_inf = json.load(open(kap))["kappa"] * -math.log(math.cos(math.pi / (n + 1)))
+                rem = math.log(pd["rel"] / 1e-6)
+                lo, hi = pd["cycles"] + rem / r_last, pd["cycles"] + rem / r_inf
+                msc = pj["ms_per_cycle_device"]
+                proj["bracket_from_measured"] = {
+                    "cycles": [lo, hi], "seconds": [lo * msc * 1e-3, hi * msc * 1e-3],
+                    "ms_per_cycle": msc, "rate_last_segment": r_last, "rate_asymptotic": r_inf,
+                    "basis": "measured trajectory to 3.0 M cycles + the remaining factor at the last segment's "
+                             "rate (lower) and at the cycle's asymptotic smooth-mode rate (upper; "
+                             "profiles/r02_smooth_rate.md)"}
         if classic_ms:
             ccyc = fit["classic"]["cycles_16384"]
             proj["classic_sweeps_projected"] = ccyc
