@@ -614,6 +614,18 @@ res1c_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
   if (lane == 31) s_e[cs.c & 1][w][1] = x[C - 1];
   __syncthreads();
   T gl[D], gr[D];  // ghosts: gl[m-1] = point -m, gr[m-1] = point C-1+m
+  // software-pipelined exchange (as RES1W): the shuffles a group needs are issued at the end of the
+  // previous group, in the same basic block as its last sub-iteration, into pa / pb; a group only
+  // applies the frozen-halo selects to them
+  T pa[D], pb[D];
+  auto issue = [&] {
+#pragma unroll
+    for (int m = 1; m <= D; ++m) {
+      pa[m - 1] = __shfl_up_sync(FULL, x[C - 1 - (m - 1) % C], (m - 1) / C + 1);
+      pb[m - 1] = __shfl_down_sync(FULL, x[(m - 1) % C], (m - 1) / C + 1);
+    }
+  };
+  issue();
   for (;;) {
     const long long cyc = cs.c;
     const int par = (int)(cyc & 1);
@@ -626,15 +638,14 @@ res1c_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
     T xs[C];  // the snapshot x_c (returned if the cycle's test stops the solve)
 #pragma unroll
     for (int c = 0; c < C; ++c) xs[c] = x[c];
-    // ghosts of depth d from the neighbouring lanes; the frozen ones take the halo
+    // ghosts of depth d from the neighbouring lanes (shuffled by the last issue()); the frozen ones
+    // take the halo
     auto exch = [&](auto dd) {
       constexpr int d = decltype(dd)::value;
 #pragma unroll
       for (int m = 1; m <= d; ++m) {
-        const T a = __shfl_up_sync(FULL, x[C - 1 - (m - 1) % C], (m - 1) / C + 1);
-        const T b = __shfl_down_sync(FULL, x[(m - 1) % C], (m - 1) / C + 1);
-        gl[m - 1] = fl[m - 1] ? hl : a;
-        gr[m - 1] = fr[m - 1] ? hr : b;
+        gl[m - 1] = fl[m - 1] ? hl : pa[m - 1];
+        gr[m - 1] = fr[m - 1] ? hr : pb[m - 1];
       }
     };
     double acc = 0.0;
@@ -685,6 +696,7 @@ res1c_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
           gr[m - 1] = ngr[m - 1];
         }
       }
+      issue();  // the next group's exchange (or the next cycle's first)
     };
     using I1 = std::integral_constant<int, 1>;
     using ID = std::integral_constant<int, D>;
@@ -699,14 +711,13 @@ res1c_kernel(T* __restrict__ X0, T* __restrict__ X1, const T* __restrict__ Q, in
       else group(ID{}, std::false_type{});
       s = D;
     }
-    int step = 16;  // butterfly of acc, one step per following group
-#pragma unroll 1
+    int step = 16;  // butterfly of acc, one step per following group (shuffle before, predicated add after)
+#pragma unroll 2
     for (; s < kk; s += D) {
+      const double pbf = __shfl_xor_sync(FULL, acc, step ? step : 16);
       group(ID{}, std::false_type{});
-      if (step) {
-        acc += __shfl_xor_sync(FULL, acc, step);
-        step >>= 1;
-      }
+      acc = step ? acc + pbf : acc;
+      step >>= 1;
     }
     for (; step; step >>= 1) acc += __shfl_xor_sync(FULL, acc, step);
     if (lane == 0) {
